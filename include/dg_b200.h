@@ -1,0 +1,223 @@
+/* dg_b200.h -- C-ABI of the B200-native straightest-geodesic tracer (libdigeo_b200.so).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++/torch types. The host
+ * C++ layer in include/digeo/ (same names and semantics as the reference's
+ * proj/include/digeo/) is a thin shim over these entry points, and INTEGRATION.md shows
+ * the binding a maintainer of the reference would add at each call site.
+ *
+ * Reference call sites replaced (paths relative to the reference tree):
+ *   dg_mesh_derive        <- Mesh::build derived arrays        proj/src/mesh.cpp:34-130
+ *   dg_mesh_create        <- (device mirror of) class Mesh     proj/include/digeo/mesh.hpp:40-83
+ *   dg_trace_batch        <- trace_batch / trace_batch_serial  proj/src/tracer.cpp:596-610
+ *                            (OpenMP loop at :600 over run_one :578 -> Kernel<S>::run :490)
+ *   dg_transition         <- geodesic_step, transport_over_edge, transport_over_vertex,
+ *                            boundary_continue                 proj/src/tracer.cpp:630-735
+ *   dg_ep_jacobians       <- ep_jacobians (+ frames)           proj/src/diff.cpp:13-66
+ *   dg_ep_backward        <- ep_jacobians + pullback_ambient   proj/src/diff.cpp:44-66,328-354
+ *   dg_gfd_jacobians      <- gfd_batched_many / gfd_batched / gfd_jacobian_v/p
+ *                                                              proj/src/diff.cpp:208-326
+ *   dg_pullback           <- pullback / pullback_ambient       proj/src/diff.cpp:328-354
+ *
+ * All functions return DG_OK (0) or a DG_ERR_* code, never throw and never abort;
+ * dg_last_error() gives the message of the last failure on the calling thread.
+ * Per-element failures of a batch are NOT errors of the call: they are reported in the
+ * status / stall bytes of that element (reference: tracer.cpp:584-591).
+ * There is no CPU fallback: every compute entry point fails with DG_ERR_NO_DEVICE when no
+ * CUDA device is usable. dg_mesh_derive is host-only by design (it mirrors Mesh::build,
+ * which is build-once host code in the reference too).
+ */
+#ifndef DG_B200_H
+#define DG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_API __attribute__((visibility("default")))
+
+typedef struct dg_mesh dg_mesh;
+
+/* ---- return codes (mapped 1:1 to the reference's exception classes, geometry.hpp:187-200) */
+enum {
+  DG_OK = 0,
+  DG_ERR_INVALID_ARGS = 1,         /* digeo::InvalidArgs */
+  DG_ERR_CUDA = 2,                 /* CUDA runtime failure */
+  DG_ERR_PARSE = 3,                /* digeo::ParseError (vertex index out of range) */
+  DG_ERR_NON_MANIFOLD = 4,         /* digeo::NonManifoldError */
+  DG_ERR_DEGENERATE_FACE = 5,      /* digeo::DegenerateFaceError */
+  DG_ERR_DEGENERATE_DIRECTION = 6, /* digeo::DegenerateDirection */
+  DG_ERR_GFD = 7,                  /* plain digeo::Error from diff.cpp:123,184 */
+  DG_ERR_NO_DEVICE = 8,            /* no usable CUDA device: there is no CPU fallback */
+  DG_ERR_NUMERICAL_STALL = 10,     /* digeo::NumericalStall (single-call wrappers) */
+  DG_ERR_BOUNDARY_HIT = 11         /* digeo::BoundaryHit (transport_over_vertex) */
+};
+
+/* ---- per-element codes */
+enum { DG_TERM_LENGTH_REACHED = 0, DG_TERM_BOUNDARY = 1, DG_TERM_MAX_STEPS = 2 };
+enum { DG_STATUS_OK = 0, DG_STATUS_STALLED = 1 };
+enum {
+  DG_STALL_NONE = 0,
+  DG_STALL_DEGENERATE_DIRECTION = 1, /* "degenerate direction in face"            tracer.cpp:183 */
+  DG_STALL_NO_EXIT = 2,              /* "no positive exit parameter"              tracer.cpp:197 */
+  DG_STALL_NORMAL_DIRECTION = 3,     /* "initial direction is normal to the anchor face" :474 */
+  DG_STALL_FACE_RANGE = 4,           /* "trace: start face out of range"          tracer.cpp:459 */
+  DG_STALL_BARY_RANGE = 5            /* "trace: start barycentric coordinates not in the simplex" :461 */
+};
+/* StepEvent, tracer.hpp:52 */
+enum { DG_EVENT_ADVANCED = 0, DG_EVENT_CROSSED_EDGE = 1, DG_EVENT_CROSSED_VERTEX = 2,
+       DG_EVENT_BOUNDARY_SLIDE = 3, DG_EVENT_BOUNDARY_STOP = 4 };
+
+enum { DG_MEM_HOST = 0, DG_MEM_DEVICE = 1 };
+/* arithmetic lane of the f64 tracer */
+enum {
+  DG_LANE_FAST = 0,  /* FMA-contracted FP64 (default): identical face sequences on non-degenerate
+                        queries, positions within 1e-9 x bbox diagonal of the reference */
+  DG_LANE_EXACT = 1  /* no contraction, reference operation order: bit-identical to the reference
+                        CPU build on traces that never take a vertex branch (no libm calls) */
+};
+
+DG_API const char* dg_last_error(void);
+DG_API const char* dg_version(void);
+DG_API int dg_device_count(void);          /* 0 when no CUDA device / driver */
+DG_API int dg_set_device(int ordinal);     /* device used by subsequently created meshes */
+DG_API int dg_device_sm_count(void);
+
+/* ---- mesh ------------------------------------------------------------------------------
+ * dg_mesh_derive: host-side restatement of Mesh::build (mesh.cpp:34-130). Validates the
+ * triangle soup and fills the derived arrays (any output pointer may be NULL):
+ *   adj[3nf] (-1 = boundary; local edge k is opposite corner k), fnormal[3nf] unit,
+ *   farea[nf], vangle[nv] total interior angle, varea[nv], vboundary[nv],
+ *   csr_off[nv+1]/csr_list[3nf] vertex->faces in face order, mean edge length, total area.
+ * err_index receives the offending face (or, for non-manifold edges, the smaller vertex). */
+DG_API int dg_mesh_derive(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf,
+                          int32_t* adj, double* fnormal, double* farea, double* vangle,
+                          double* varea, uint8_t* vboundary, int32_t* csr_off,
+                          int32_t* csr_list, double* mean_edge, double* total_area,
+                          int64_t* err_index);
+
+/* Uploads an immutable mesh (host pointers) into the device SoA layout described in
+ * DESIGN.md. All arrays are required and must come from dg_mesh_derive (or Mesh::build). */
+DG_API int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf,
+                          const int32_t* adj, const double* fnormal, const double* vangle,
+                          const uint8_t* vboundary, const int32_t* csr_off,
+                          const int32_t* csr_list, dg_mesh** out);
+DG_API void dg_mesh_destroy(dg_mesh* m);
+DG_API int32_t dg_mesh_face_count(const dg_mesh* m);
+DG_API int32_t dg_mesh_vertex_count(const dg_mesh* m);
+DG_API int64_t dg_mesh_device_bytes(const dg_mesh* m);
+DG_API int dg_mesh_device(const dg_mesh* m);
+
+/* ---- forward tracing ------------------------------------------------------------------- */
+typedef struct dg_trace_cfg {
+  int32_t max_steps;             /* 0: 10*sqrt(F)+100 (tracer.cpp:543) */
+  uint8_t hole_avoidance;
+  uint8_t want_transport_matrix;
+  uint8_t use_f32;               /* run the stepping arithmetic in single precision */
+  uint8_t lane;                  /* DG_LANE_FAST / DG_LANE_EXACT (f64 only) */
+  uint8_t memory;                /* DG_MEM_HOST: pointers are host memory, staged by the library
+                                    DG_MEM_DEVICE: pointers are device memory on the mesh's GPU */
+  uint8_t sort_by_face;          /* schedule queries in start-face order (results stay at request index) */
+  uint8_t refill_min;            /* idle lanes a warp waits for before it steals work (0 = default 1) */
+  uint8_t blocks_per_sm;         /* resident CTAs per SM of the persistent grid (0 = occupancy query) */
+  void* stream;                  /* cudaStream_t to launch on. DG_MEM_HOST: NULL = the mesh's private
+                                    stream, the call returns when the results are in host memory.
+                                    DG_MEM_DEVICE: NULL = the CUDA default stream; the call is
+                                    asynchronous on that stream. */
+} dg_trace_cfg;
+
+typedef struct dg_trace_in {
+  const int32_t* face;     /* [n]   start face */
+  const double* bary;      /* [3n]  start barycentrics */
+  const double* dir;       /* [3n]  ambient tangent vector; its norm is the requested length */
+  const double* payload;   /* [3n] or NULL; an all-zero row means "no payload" (tracer.cpp:582) */
+} dg_trace_in;
+
+/* Every pointer may be NULL (that output is then skipped). */
+typedef struct dg_trace_out {
+  int32_t* face;        /* [n]  final face (-1 for a rejected start, as a default GeodesicTrace) */
+  double* bary;         /* [3n] final barycentrics, renormalised as tracer.cpp:75-82 */
+  double* dir;          /* [3n] final unit direction (0 for zero-length requests) */
+  double* traced;       /* [n]  traced length */
+  double* requested;    /* [n]  requested length */
+  uint8_t* term;        /* [n]  DG_TERM_* */
+  uint8_t* status;      /* [n]  DG_STATUS_* */
+  uint8_t* stall;       /* [n]  DG_STALL_* */
+  double* payload;      /* [3n] transported payload (rows of payload-free elements are 0) */
+  double* transport;    /* [9n] row-major transport matrix (want_transport_matrix) */
+  int32_t* npoints;     /* [n]  number of polyline points the trace emits */
+  int32_t* crossings;   /* [n]  face-to-face transitions executed (edge crossings + fan faces) */
+  uint64_t* total_crossings; /* [1] sum of crossings over the batch (overwritten) */
+  /* polyline recording: pass offsets from an exclusive scan of npoints of a previous call */
+  const int64_t* poly_offsets; /* [n]  first slot of trace i; recording is on iff non-NULL */
+  int64_t poly_total;   /* number of slots in the three poly_* arrays (sum of npoints) */
+  int32_t* poly_face;   /* [total] */
+  double* poly_bary;    /* [3 total] */
+  double* poly_seg;     /* [total] length of the segment ENDING at this point (0 at the start point) */
+} dg_trace_out;
+
+DG_API int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in,
+                          const dg_trace_cfg* cfg, dg_trace_out* out);
+
+/* Registers per thread, resident CTAs per SM and CTA size of a tracer kernel variant
+ * (full = payload / transport matrix / hole avoidance / polyline support compiled in). */
+DG_API void dg_trace_kernel_info(int use_f32, int full, int* regs, int* blocks_per_sm,
+                                 int* block_threads);
+
+/* Single-transition operations on n independent states (host pointers).
+ * which: 0 geodesic_step (uses remaining[], writes step_length/finished/event)
+ *        1 transport_over_edge   2 transport_over_vertex   3 boundary_continue
+ * rc[i] receives DG_OK or the DG_ERR_* the reference would have thrown for element i. */
+DG_API int dg_transition(const dg_mesh* mesh, int which, int64_t n, const int32_t* face,
+                         const double* bary, const double* v, const double* remaining,
+                         int hole_avoidance, int32_t* out_face, double* out_bary, double* out_v,
+                         double* step_length, uint8_t* finished, uint8_t* event, uint8_t* stall,
+                         int32_t* rc);
+
+/* ---- differentials --------------------------------------------------------------------- */
+#define DG_FRAME_DOUBLES 33
+/* frames block per sample: e_par, e_perp, normal (frame_in_v) | u_hat, v_hat, pinv_row0,
+ * pinv_row1 (frame_in_p) | the same four for frame_out */
+
+typedef struct dg_diff_cfg {
+  uint8_t memory;       /* DG_MEM_HOST / DG_MEM_DEVICE for all pointers of the call */
+  uint8_t lane;         /* tracer lane used by GFD re-traces */
+  uint8_t reserved[6];
+  void* stream;
+  int32_t max_steps;    /* GFD re-traces; 0 = default */
+} dg_diff_cfg;
+
+/* Extrinsic-proxy Jacobians for n samples. rot[9n] = rotation_ep (row-major), frames
+ * [DG_FRAME_DOUBLES n]; either may be NULL. Fails with DG_ERR_DEGENERATE_DIRECTION (and
+ * *err_index = first offending sample) when |v| < 1e-12 or v is normal to its face. */
+DG_API int dg_ep_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face,
+                           const double* bary, const double* v, const int32_t* end_face,
+                           const double* end_bary, const double* end_dir, const dg_diff_cfg* cfg,
+                           double* rot, double* frames, int64_t* err_index);
+
+/* Fused EP backward: grad_v[3n] = pullback_ambient(g, ep_jacobians(...)).grad_v; grad_p is
+ * identically zero for EP and is only written when non-NULL. */
+DG_API int dg_ep_backward(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* v,
+                          const int32_t* end_face, const double* end_dir, const double* g,
+                          const dg_diff_cfg* cfg, double* grad_v, double* grad_p,
+                          int64_t* err_index);
+
+/* Geodesic finite differences for n samples in two batched trace rounds (+ a third for
+ * one-sided fallbacks). jv/jp[4n] row-major 2x2 (a b c d), degraded[4n] = degraded_v[0..1],
+ * degraded_p[0..1]; frames may be NULL. If g != NULL also writes grad_v/grad_p[3n]
+ * (pullback_ambient). base_* (optional, may all be NULL) receive the base traces' end states.
+ * Whole-call failures as in the reference: DG_ERR_DEGENERATE_DIRECTION (frames),
+ * DG_ERR_GFD ("gfd: the base trace did not reach its requested length",
+ * "gfd: start-point perturbation seeds failed to trace"). */
+DG_API int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face,
+                            const double* bary, const double* v, double eps_v, double eps_p,
+                            const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
+                            uint8_t* degraded, double* frames, double* grad_v, double* grad_p,
+                            int32_t* base_face, double* base_bary, double* base_dir,
+                            int64_t* err_index);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DG_B200_H */

@@ -1,0 +1,289 @@
+"""Array-level mirror of the reference's operator interface for this path, over the C-ABI.
+
+Names and argument meaning follow proj/include/digeo/{mesh,tracer,diff}.hpp (Mesh::build,
+trace_batch, geodesic_step ..., ep_jacobians, gfd_batched_many, pullback_ambient); the
+object-level C++ mirror lives in include/digeo/. Inputs/outputs are numpy arrays (host mode:
+the library stages them) or torch CUDA tensors (device mode: zero-copy, asynchronous on the
+current torch stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import capi
+from .capi import DgError, DiffCfg, TraceCfg, TraceIn, TraceOut, check, lib, ptr
+
+
+def _f64(a, shape=None):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a.reshape(shape) if shape else a
+
+
+def _i32(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _is_torch(a):
+    return a is not None and not isinstance(a, np.ndarray) and hasattr(a, "data_ptr")
+
+
+@dataclass
+class TraceResult:
+    face: np.ndarray
+    bary: np.ndarray
+    dir: np.ndarray
+    traced: np.ndarray
+    requested: np.ndarray
+    term: np.ndarray       # 0 LengthReached, 1 Boundary, 2 MaxSteps
+    status: np.ndarray     # 0 Ok, 1 Stalled
+    stall: np.ndarray      # DG_STALL_*
+    npoints: np.ndarray
+    crossings: np.ndarray
+    total_crossings: int = 0
+    payload: np.ndarray | None = None
+    has_payload: np.ndarray | None = None
+    q: np.ndarray | None = None
+    poly_offsets: np.ndarray | None = None
+    poly_face: np.ndarray | None = None
+    poly_bary: np.ndarray | None = None
+    poly_seg: np.ndarray | None = None
+    errors: list = field(default_factory=list)
+
+
+class Mesh:
+    """Immutable triangle mesh: host-side derived arrays (Mesh::build, mesh.cpp:34-130) plus
+    the GPU-resident fat-record store (dg_mesh_create)."""
+
+    def __init__(self, xyz, tri, device=None, upload=True):
+        L = lib()
+        self.xyz = _f64(xyz).reshape(-1, 3)
+        self.tri = _i32(tri).reshape(-1, 3)
+        nv, nf = len(self.xyz), len(self.tri)
+        self.nv, self.nf = nv, nf
+        self.adj = np.empty((nf, 3), np.int32)
+        self.fnormal = np.empty((nf, 3))
+        self.farea = np.empty(nf)
+        self.vangle = np.empty(nv)
+        self.varea = np.empty(nv)
+        self.vboundary = np.empty(nv, np.uint8)
+        self.csr_off = np.empty(nv + 1, np.int32)
+        self.csr_list = np.empty(3 * nf, np.int32)
+        me, ta, ei = C.c_double(0), C.c_double(0), C.c_int64(-1)
+        check(L.dg_mesh_derive(ptr(self.xyz), nv, ptr(self.tri), nf, ptr(self.adj), ptr(self.fnormal),
+                               ptr(self.farea), ptr(self.vangle), ptr(self.varea), ptr(self.vboundary),
+                               ptr(self.csr_off), ptr(self.csr_list), C.addressof(me), C.addressof(ta),
+                               C.addressof(ei)), ei)
+        self.mean_edge = me.value
+        self.total_area = ta.value
+        self.h = None
+        if upload:
+            self.upload(device)
+
+    build = classmethod(lambda cls, xyz, tri, **kw: cls(xyz, tri, **kw))
+
+    def upload(self, device=None):
+        L = lib()
+        capi.require_device()
+        if device is not None:
+            check(L.dg_set_device(int(device)))
+        h = C.c_void_p(0)
+        check(L.dg_mesh_create(ptr(self.xyz), self.nv, ptr(self.tri), self.nf, ptr(self.adj), ptr(self.fnormal),
+                               ptr(self.vangle), ptr(self.vboundary), ptr(self.csr_off), ptr(self.csr_list),
+                               C.addressof(h)))
+        self.h = h
+        return self
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().dg_mesh_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self):
+        return lib().dg_mesh_device_bytes(self.h)
+
+    def default_max_steps(self):
+        return int(10.0 * np.sqrt(float(self.nf))) + 100
+
+    def default_gfd_eps(self):
+        return 1e-4 * self.mean_edge
+
+    def embed(self, face, bary):
+        X = self.xyz[self.tri[face]]
+        return np.einsum("nk,nkd->nd", bary, X)
+
+    def _handle(self):
+        if not self.h:
+            raise DgError(capi.DG_ERR_NO_DEVICE, "mesh is not resident on a GPU (there is no CPU fallback)")
+        return self.h
+
+    # ------------------------------------------------------------------ forward tracing
+    def trace_batch(self, face, bary, dirs, payload=None, max_steps=0, hole_avoidance=False, want_q=False,
+                    record_polyline=False, use_f32=False, sort_by_face=False, refill_min=0, blocks_per_sm=0,
+                    out=None):
+        """trace_batch (tracer.cpp:596) on host arrays; results at the request index. `out`: a
+        TraceResult of a previous call of the same size whose (e.g. pinned) arrays are reused."""
+        h = self._handle()
+        face, bary, dirs, payload = _i32(face), _f64(bary), _f64(dirs), _f64(payload)
+        n = len(face)
+        if bary.size != 3 * n or dirs.size != 3 * n:
+            raise DgError(1, "trace_batch: starts and dirs differ in length")
+        if payload is not None and payload.size != 3 * n:
+            raise DgError(1, "trace_batch: payloads must be empty or match the batch size")
+        r = out if out is not None else TraceResult(
+            face=np.empty(n, np.int32), bary=np.empty((n, 3)), dir=np.empty((n, 3)),
+            traced=np.empty(n), requested=np.empty(n), term=np.empty(n, np.uint8),
+            status=np.empty(n, np.uint8), stall=np.empty(n, np.uint8),
+            npoints=np.empty(n, np.int32), crossings=np.empty(n, np.int32))
+        if payload is not None:
+            r.payload = np.empty((n, 3))
+            r.has_payload = (np.square(payload.reshape(n, 3)).sum(1) > 0).astype(np.uint8)
+        if want_q:
+            r.q = np.empty((n, 9))
+        cfg = TraceCfg(max_steps=int(max_steps), hole_avoidance=int(hole_avoidance),
+                       want_transport_matrix=int(want_q), use_f32=int(use_f32), memory=capi.MEM_HOST,
+                       sort_by_face=int(sort_by_face), refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm))
+        tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), ptr(payload))
+        total = C.c_uint64(0)
+
+        def call(off, pf, pb, ps, tot):
+            out = TraceOut(ptr(r.face), ptr(r.bary), ptr(r.dir), ptr(r.traced), ptr(r.requested), ptr(r.term),
+                           ptr(r.status), ptr(r.stall), ptr(r.payload), ptr(r.q), ptr(r.npoints), ptr(r.crossings),
+                           C.addressof(total), ptr(off), tot, ptr(pf), ptr(pb), ptr(ps))
+            check(lib().dg_trace_batch(h, n, C.addressof(tin), C.addressof(cfg), C.addressof(out)))
+
+        call(None, None, None, None, 0)
+        if record_polyline:
+            # two passes: the first sized the polylines (npoints), the second writes them
+            off = np.zeros(n + 1, np.int64)
+            np.cumsum(r.npoints, out=off[1:])
+            tot = int(off[-1])
+            r.poly_offsets = off
+            r.poly_face = np.empty(tot, np.int32)
+            r.poly_bary = np.empty((tot, 3))
+            r.poly_seg = np.empty(tot)
+            if n:
+                call(off, r.poly_face, r.poly_bary, r.poly_seg, tot)
+        r.total_crossings = int(total.value)
+        r.errors = [(int(i), capi.STALL_MESSAGES[int(r.stall[i])]) for i in np.nonzero(r.status)[0]]
+        return r
+
+    def trace_batch_device(self, face, bary, dirs, out, payload=None, max_steps=0, hole_avoidance=False,
+                           want_q=False, stream=None, sort_by_face=False, refill_min=0, blocks_per_sm=0):
+        """Zero-copy entry point: every array is a torch CUDA tensor on the mesh's device;
+        `out` maps dg_trace_out field names to preallocated tensors. Asynchronous on `stream`."""
+        import torch
+        h = self._handle()
+        n = int(face.numel())
+        cfg = TraceCfg(max_steps=int(max_steps), hole_avoidance=int(hole_avoidance),
+                       want_transport_matrix=int(want_q), memory=capi.MEM_DEVICE, sort_by_face=int(sort_by_face),
+                       refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm),
+                       stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
+        tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), ptr(payload))
+        o = TraceOut()
+        for k, v in out.items():
+            if k == "poly_total":
+                o.poly_total = int(v)
+            else:
+                setattr(o, k, ptr(v))
+        check(lib().dg_trace_batch(h, n, C.addressof(tin), C.addressof(cfg), C.addressof(o)))
+
+    # ------------------------------------------------------- single-transition operations
+    def transition(self, which, face, bary, v, remaining=None, hole_avoidance=False):
+        """which: 0 geodesic_step, 1 transport_over_edge, 2 transport_over_vertex,
+        3 boundary_continue (tracer.cpp:630-735), on n independent states."""
+        h = self._handle()
+        face, bary, v = _i32(np.atleast_1d(face)), _f64(bary).reshape(-1, 3), _f64(v).reshape(-1, 3)
+        n = len(face)
+        rem = _f64(np.broadcast_to(np.asarray(0.0 if remaining is None else remaining, float), (n,)))
+        o = dict(face=np.empty(n, np.int32), bary=np.empty((n, 3)), v=np.empty((n, 3)), step_length=np.zeros(n),
+                 finished=np.zeros(n, np.uint8), event=np.zeros(n, np.uint8), stall=np.zeros(n, np.uint8),
+                 rc=np.zeros(n, np.int32))
+        check(lib().dg_transition(h, int(which), n, ptr(face), ptr(bary), ptr(v), ptr(rem), int(hole_avoidance),
+                                  ptr(o["face"]), ptr(o["bary"]), ptr(o["v"]), ptr(o["step_length"]),
+                                  ptr(o["finished"]), ptr(o["event"]), ptr(o["stall"]), ptr(o["rc"])))
+        return o
+
+    # --------------------------------------------------------------------- differentials
+    def ep(self, face, bary, v, end_face, end_bary, end_dir, g=None):
+        """ep_jacobians (+ pullback_ambient when g is given), diff.cpp:44-66, :347-354."""
+        h = self._handle()
+        face, end_face = _i32(face), _i32(end_face)
+        n = len(face)
+        bary, v, end_bary, end_dir, g = _f64(bary), _f64(v), _f64(end_bary), _f64(end_dir), _f64(g)
+        out = dict(rot=np.empty((n, 9)), frames=np.empty((n, capi.FRAME_DOUBLES)), grad_v=np.zeros((n, 3)),
+                   grad_p=np.zeros((n, 3)))
+        ei = C.c_int64(-1)
+        cfg = DiffCfg(memory=capi.MEM_HOST)
+        check(lib().dg_ep_jacobians(h, n, ptr(face), ptr(bary), ptr(v), ptr(end_face), ptr(end_bary), ptr(end_dir),
+                                    C.addressof(cfg), ptr(out["rot"]), ptr(out["frames"]), C.addressof(ei)), ei)
+        if g is not None:
+            check(lib().dg_ep_backward(h, n, ptr(face), ptr(v), ptr(end_face), ptr(end_dir), ptr(g),
+                                       C.addressof(cfg), ptr(out["grad_v"]), ptr(out["grad_p"]), C.addressof(ei)), ei)
+        return out
+
+    def ep_backward(self, face, v, end_face, end_dir, g, grad_v=None):
+        """Fused ep_jacobians + pullback_ambient on host arrays: returns grad_v (grad_p == 0)."""
+        face, end_face = _i32(face), _i32(end_face)
+        n = len(face)
+        v, end_dir, g = _f64(v), _f64(end_dir), _f64(g)
+        if grad_v is None:
+            grad_v = np.empty((n, 3))
+        ei = C.c_int64(-1)
+        cfg = DiffCfg(memory=capi.MEM_HOST)
+        check(lib().dg_ep_backward(self._handle(), n, ptr(face), ptr(v), ptr(end_face), ptr(end_dir), ptr(g),
+                                   C.addressof(cfg), ptr(grad_v), None, C.addressof(ei)), ei)
+        return grad_v
+
+    def ep_backward_device(self, face, v, end_face, end_dir, g, grad_v, grad_p=None, stream=None):
+        import torch
+        cfg = DiffCfg(memory=capi.MEM_DEVICE,
+                      stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
+        ei = C.c_int64(-1)
+        check(lib().dg_ep_backward(self._handle(), int(face.numel()), ptr(face), ptr(v), ptr(end_face), ptr(end_dir),
+                                   ptr(g), C.addressof(cfg), ptr(grad_v), ptr(grad_p), C.addressof(ei)), ei)
+
+    def gfd(self, face, bary, v, eps_v=None, eps_p=None, g=None, max_steps=0):
+        """gfd_batched_many (+ pullback_ambient when g is given), diff.cpp:273-326."""
+        h = self._handle()
+        face = _i32(face)
+        n = len(face)
+        bary, v, g = _f64(bary), _f64(v), _f64(g)
+        eps = self.default_gfd_eps()
+        eps_v = eps if eps_v is None else eps_v
+        eps_p = eps if eps_p is None else eps_p
+        out = dict(jv=np.zeros((n, 4)), jp=np.zeros((n, 4)), degraded=np.zeros((n, 4), np.uint8),
+                   frames=np.zeros((n, capi.FRAME_DOUBLES)), grad_v=np.zeros((n, 3)), grad_p=np.zeros((n, 3)),
+                   base_face=np.empty(n, np.int32), base_bary=np.empty((n, 3)), base_dir=np.empty((n, 3)))
+        ei = C.c_int64(-1)
+        cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps))
+        check(lib().dg_gfd_jacobians(h, n, ptr(face), ptr(bary), ptr(v), float(eps_v), float(eps_p), ptr(g),
+                                     C.addressof(cfg), ptr(out["jv"]), ptr(out["jp"]), ptr(out["degraded"]),
+                                     ptr(out["frames"]), ptr(out["grad_v"]) if g is not None else None,
+                                     ptr(out["grad_p"]) if g is not None else None, ptr(out["base_face"]),
+                                     ptr(out["base_bary"]), ptr(out["base_dir"]), C.addressof(ei)), ei)
+        return out
+
+    def gfd_device(self, face, bary, v, eps_v, eps_p, g, jv, jp, grad_v=None, grad_p=None, degraded=None,
+                   stream=None, max_steps=0):
+        import torch
+        cfg = DiffCfg(memory=capi.MEM_DEVICE, max_steps=int(max_steps),
+                      stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
+        ei = C.c_int64(-1)
+        check(lib().dg_gfd_jacobians(self._handle(), int(face.numel()), ptr(face), ptr(bary), ptr(v), float(eps_v),
+                                     float(eps_p), ptr(g), C.addressof(cfg), ptr(jv), ptr(jp), ptr(degraded), None,
+                                     ptr(grad_v), ptr(grad_p), None, None, None, C.addressof(ei)), ei)
+
+
+def kernel_info(use_f32=False, full=False):
+    regs, bps, bt = C.c_int(0), C.c_int(0), C.c_int(0)
+    lib().dg_trace_kernel_info(int(use_f32), int(full), C.addressof(regs), C.addressof(bps), C.addressof(bt))
+    return dict(registers=regs.value, blocks_per_sm=bps.value, block_threads=bt.value)

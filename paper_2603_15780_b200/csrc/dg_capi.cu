@@ -1,0 +1,401 @@
+// C-ABI entry points: devices, mesh store and forward tracing (include/dg_b200.h).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "dg_capi_common.hpp"
+
+namespace dgapi {
+
+std::string& last_error() {
+  thread_local std::string s;
+  return s;
+}
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  last_error() = buf;
+  return code;
+}
+int fail_cuda(cudaError_t e, const char* where) {
+  cudaGetLastError();  // clear the sticky-free error state
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+    return fail(DG_ERR_NO_DEVICE, "no usable CUDA device (%s): there is no CPU fallback", cudaGetErrorString(e));
+  return fail(DG_ERR_CUDA, "CUDA error %s at %s", cudaGetErrorString(e), where);
+}
+
+}  // namespace dgapi
+
+using namespace dgapi;
+
+namespace {
+
+thread_local int g_device = 0;
+
+__global__ void build_records_kernel(const double* __restrict__ xyz, const int32_t* __restrict__ tri,
+                                     const int32_t* __restrict__ adj, int32_t nf, dg::FaceRec* rec) {
+  int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  dg::FaceRec r;
+  for (int k = 0; k < 3; ++k) {
+    int v = tri[3 * f + k];
+    r.v[k] = v;
+    r.adj[k] = adj[3 * f + k];
+    r.x[3 * k + 0] = xyz[3 * size_t(v) + 0];
+    r.x[3 * k + 1] = xyz[3 * size_t(v) + 1];
+    r.x[3 * k + 2] = xyz[3 * size_t(v) + 2];
+  }
+  rec[f] = r;
+}
+
+__global__ void iota_kernel(int32_t* a, int64_t n) {
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i < n) a[i] = int32_t(i);
+}
+
+}  // namespace
+
+namespace dg {
+cudaError_t launch_build_records(const double* xyz, const int32_t* tri, const int32_t* adj, int32_t nf,
+                                 FaceRec* rec, cudaStream_t stream) {
+  if (nf <= 0) return cudaSuccess;
+  build_records_kernel<<<(nf + 255) / 256, 256, 0, stream>>>(xyz, tri, adj, nf, rec);
+  return cudaGetLastError();
+}
+}  // namespace dg
+
+extern "C" {
+
+const char* dg_last_error(void) { return last_error().c_str(); }
+const char* dg_version(void) { return "digeo-b200 0.1 (sm_100a)"; }
+
+int dg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int dg_set_device(int ordinal) {
+  int n = dg_device_count();
+  if (n == 0) return fail(DG_ERR_NO_DEVICE, "no usable CUDA device: there is no CPU fallback");
+  if (ordinal < 0 || ordinal >= n) return fail(DG_ERR_INVALID_ARGS, "dg_set_device: ordinal %d out of range [0,%d)", ordinal, n);
+  g_device = ordinal;
+  return DG_OK;
+}
+
+int dg_device_sm_count(void) {
+  if (dg_device_count() == 0) return 0;
+  int sm = 0;
+  if (cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, g_device) != cudaSuccess) return 0;
+  return sm;
+}
+
+// ------------------------------------------------------------------------------------ mesh
+
+// Host restatement of Mesh::build (proj/src/mesh.cpp:34-130). The reference matches edges
+// through a std::map keyed by sorted vertex pairs; here the 3F half-edges are sorted by the
+// same key, which visits the edges in the map's order (so the mean edge length is summed in
+// the same order) in O(F log F) without node allocations.
+int dg_mesh_derive(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf, int32_t* adj,
+                   double* fnormal, double* farea, double* vangle, double* varea, uint8_t* vboundary,
+                   int32_t* csr_off, int32_t* csr_list, double* mean_edge, double* total_area,
+                   int64_t* err_index) {
+  if (err_index) *err_index = -1;
+  if (nv < 0 || nf < 0 || (nv > 0 && !xyz) || (nf > 0 && !tri))
+    return fail(DG_ERR_INVALID_ARGS, "dg_mesh_derive: null or negative-size input");
+  using V = dg::V3<double>;
+  auto P = [&](int v) { return V{xyz[3 * size_t(v)], xyz[3 * size_t(v) + 1], xyz[3 * size_t(v) + 2]}; };
+
+  for (int f = 0; f < nf; ++f) {  // mesh.cpp:41-49
+    const int32_t* c = tri + 3 * size_t(f);
+    for (int k = 0; k < 3; ++k)
+      if (c[k] < 0 || c[k] >= nv) {
+        if (err_index) *err_index = f;
+        return fail(DG_ERR_PARSE, "face %d references vertex out of range", f);
+      }
+    if (c[0] == c[1] || c[1] == c[2] || c[0] == c[2]) {
+      if (err_index) *err_index = f;
+      return fail(DG_ERR_DEGENERATE_FACE, "face %d has repeated vertices", f);
+    }
+  }
+
+  std::vector<double> area_store;
+  if (!farea && varea) { area_store.resize(nf); farea = area_store.data(); }
+  double area_sum = 0;
+  for (int f = 0; f < nf; ++f) {  // mesh.cpp:55-68
+    const int32_t* c = tri + 3 * size_t(f);
+    V e1 = P(c[1]) - P(c[0]);
+    V e2 = P(c[2]) - P(c[0]);
+    V n = dg::cross(e1, e2);
+    double a2 = dg::norm(n);
+    double longest2 = std::max({dg::norm2(e1), dg::norm2(e2), dg::norm2(P(c[2]) - P(c[1]))});
+    if (a2 <= 1e-14 * longest2 || longest2 == 0.0) {
+      if (err_index) *err_index = f;
+      return fail(DG_ERR_DEGENERATE_FACE, "face %d has zero area", f);
+    }
+    if (fnormal) {
+      V u = n / a2;
+      fnormal[3 * size_t(f)] = u.x; fnormal[3 * size_t(f) + 1] = u.y; fnormal[3 * size_t(f) + 2] = u.z;
+    }
+    double a = 0.5 * a2;
+    if (farea) farea[f] = a;
+    area_sum += a;
+  }
+  if (total_area) *total_area = area_sum;
+
+  // adjacency, mesh.cpp:71-90
+  struct HalfEdge { uint64_t key; int32_t slot; };  // slot = 3 f + k (scan order of the reference)
+  std::vector<HalfEdge> he(size_t(3) * nf);
+  for (int f = 0; f < nf; ++f)
+    for (int k = 0; k < 3; ++k) {
+      int a = tri[3 * size_t(f) + (k + 1) % 3], b = tri[3 * size_t(f) + (k + 2) % 3];
+      uint64_t lo = uint64_t(std::min(a, b)), hi = uint64_t(std::max(a, b));
+      he[3 * size_t(f) + k] = {(lo << 32) | hi, int32_t(3 * f + k)};
+    }
+  std::sort(he.begin(), he.end(), [](const HalfEdge& x, const HalfEdge& y) {
+    return x.key != y.key ? x.key < y.key : x.slot < y.slot;
+  });
+  if (adj) std::fill(adj, adj + size_t(3) * nf, -1);
+  if (vboundary) std::fill(vboundary, vboundary + nv, uint8_t(0));
+  int64_t bad_slot = -1;
+  uint64_t bad_key = 0;
+  double edge_len_sum = 0;
+  int64_t edge_count = 0;
+  for (size_t i = 0; i < he.size();) {
+    size_t j = i;
+    while (j < he.size() && he[j].key == he[i].key) ++j;
+    const int a = int(he[i].key >> 32), b = int(he[i].key & 0xffffffffu);
+    if (j - i >= 3) {  // the reference throws when it meets the third incidence in scan order
+      if (bad_slot < 0 || he[i + 2].slot < bad_slot) { bad_slot = he[i + 2].slot; bad_key = he[i].key; }
+    } else if (j - i == 2) {
+      if (adj) { adj[he[i].slot] = he[i + 1].slot / 3; adj[he[i + 1].slot] = he[i].slot / 3; }
+    } else if (vboundary) {
+      vboundary[a] = 1; vboundary[b] = 1;
+    }
+    edge_len_sum += dg::norm(P(a) - P(b));  // mesh.cpp:96, map order
+    ++edge_count;
+    i = j;
+  }
+  if (bad_slot >= 0) {
+    if (err_index) *err_index = int64_t(bad_key >> 32);
+    return fail(DG_ERR_NON_MANIFOLD, "edge (%d,%d) incident to 3+ faces", int(bad_key >> 32), int(bad_key & 0xffffffffu));
+  }
+  if (mean_edge) *mean_edge = edge_count ? edge_len_sum / double(edge_count) : 0.0;
+
+  // total angles and vertex areas, mesh.cpp:106-115
+  if (vangle) std::fill(vangle, vangle + nv, 0.0);
+  if (varea) std::fill(varea, varea + nv, 0.0);
+  if (vangle || varea)
+    for (int f = 0; f < nf; ++f) {
+      const int32_t* c = tri + 3 * size_t(f);
+      for (int k = 0; k < 3; ++k) {
+        if (vangle) {
+          V apex = P(c[k]);
+          vangle[c[k]] += dg::angle_between(P(c[(k + 1) % 3]) - apex, P(c[(k + 2) % 3]) - apex);
+        }
+        if (varea) varea[c[k]] += farea[f] / 3.0;
+      }
+    }
+
+  // vertex -> faces CSR, mesh.cpp:118-127
+  if (csr_off) {
+    std::fill(csr_off, csr_off + nv + 1, 0);
+    for (int f = 0; f < nf; ++f)
+      for (int k = 0; k < 3; ++k) csr_off[tri[3 * size_t(f) + k] + 1]++;
+    for (int v = 0; v < nv; ++v) csr_off[v + 1] += csr_off[v];
+    if (csr_list) {
+      std::vector<int32_t> cursor(csr_off, csr_off + nv);
+      for (int f = 0; f < nf; ++f)
+        for (int k = 0; k < 3; ++k) csr_list[cursor[tri[3 * size_t(f) + k]]++] = f;
+    }
+  }
+  return DG_OK;
+}
+
+int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf, const int32_t* adj,
+                   const double* fnormal, const double* vangle, const uint8_t* vboundary,
+                   const int32_t* csr_off, const int32_t* csr_list, dg_mesh** out) {
+  if (!out) return fail(DG_ERR_INVALID_ARGS, "dg_mesh_create: null output handle");
+  *out = nullptr;
+  if (nv <= 0 || nf <= 0 || !xyz || !tri || !adj || !fnormal || !vangle || !vboundary || !csr_off || !csr_list)
+    return fail(DG_ERR_INVALID_ARGS, "dg_mesh_create: every mesh array is required (use dg_mesh_derive)");
+  if (dg_device_count() == 0) return fail(DG_ERR_NO_DEVICE, "no usable CUDA device: there is no CPU fallback");
+  DeviceGuard guard(g_device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", g_device);
+
+  dg_mesh* m = new dg_mesh;
+  m->device = g_device;
+  m->nf = nf;
+  m->nv = nv;
+  auto cleanup = [&](int rc) { dg_mesh_destroy(m); return rc; };
+  cudaError_t e;
+#define DG_TRY(expr) if ((e = (expr)) != cudaSuccess) return cleanup(fail_cuda(e, #expr))
+  DG_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, g_device));
+  DG_TRY(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  const size_t F = size_t(nf), Vn = size_t(nv);
+  DG_TRY(cudaMalloc(&m->rec, F * sizeof(dg::FaceRec)));
+  DG_TRY(cudaMalloc(&m->fnormal, 3 * F * sizeof(double)));
+  DG_TRY(cudaMalloc(&m->vangle, Vn * sizeof(double)));
+  DG_TRY(cudaMalloc(&m->csr_off, (Vn + 1) * sizeof(int32_t)));
+  DG_TRY(cudaMalloc(&m->csr_list, 3 * F * sizeof(int32_t)));
+  DG_TRY(cudaMalloc(&m->vboundary, Vn));
+  DG_TRY(cudaMalloc(&m->counters, 2 * dg_mesh::kRing * sizeof(unsigned long long)));
+  m->bytes = int64_t(F * sizeof(dg::FaceRec) + 3 * F * 8 + Vn * 8 + (Vn + 1) * 4 + 3 * F * 4 + Vn);
+
+  // indexed arrays are only needed to assemble the records
+  double* d_xyz = nullptr;
+  int32_t *d_tri = nullptr, *d_adj = nullptr;
+  DG_TRY(cudaMallocAsync(&d_xyz, 3 * Vn * sizeof(double), m->stream));
+  DG_TRY(cudaMallocAsync(&d_tri, 3 * F * sizeof(int32_t), m->stream));
+  DG_TRY(cudaMallocAsync(&d_adj, 3 * F * sizeof(int32_t), m->stream));
+  DG_TRY(cudaMemcpyAsync(d_xyz, xyz, 3 * Vn * sizeof(double), cudaMemcpyHostToDevice, m->stream));
+  DG_TRY(cudaMemcpyAsync(d_tri, tri, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
+  DG_TRY(cudaMemcpyAsync(d_adj, adj, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
+  DG_TRY(dg::launch_build_records(d_xyz, d_tri, d_adj, nf, m->rec, m->stream));
+  DG_TRY(cudaMemcpyAsync(m->fnormal, fnormal, 3 * F * sizeof(double), cudaMemcpyHostToDevice, m->stream));
+  DG_TRY(cudaMemcpyAsync(m->vangle, vangle, Vn * sizeof(double), cudaMemcpyHostToDevice, m->stream));
+  DG_TRY(cudaMemcpyAsync(m->csr_off, csr_off, (Vn + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
+  DG_TRY(cudaMemcpyAsync(m->csr_list, csr_list, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
+  DG_TRY(cudaMemcpyAsync(m->vboundary, vboundary, Vn, cudaMemcpyHostToDevice, m->stream));
+  DG_TRY(cudaMemsetAsync(m->counters, 0, 2 * dg_mesh::kRing * sizeof(unsigned long long), m->stream));
+  DG_TRY(cudaFreeAsync(d_xyz, m->stream));
+  DG_TRY(cudaFreeAsync(d_tri, m->stream));
+  DG_TRY(cudaFreeAsync(d_adj, m->stream));
+  DG_TRY(cudaStreamSynchronize(m->stream));
+#undef DG_TRY
+  *out = m;
+  return DG_OK;
+}
+
+void dg_mesh_destroy(dg_mesh* m) {
+  if (!m) return;
+  DeviceGuard guard(m->device);
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  cudaFree(m->rec); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
+  cudaFree(m->csr_list); cudaFree(m->vboundary); cudaFree(m->counters);
+  if (m->stream) cudaStreamDestroy(m->stream);
+  delete m;
+}
+
+int32_t dg_mesh_face_count(const dg_mesh* m) { return m ? m->nf : 0; }
+int32_t dg_mesh_vertex_count(const dg_mesh* m) { return m ? m->nv : 0; }
+int64_t dg_mesh_device_bytes(const dg_mesh* m) { return m ? m->bytes : 0; }
+int dg_mesh_device(const dg_mesh* m) { return m ? m->device : -1; }
+
+// ------------------------------------------------------------------------- forward tracing
+
+int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg,
+                   dg_trace_out* out) {
+  // whole-call contract violations, tracer.cpp:566-576
+  if (!mesh) return fail(DG_ERR_INVALID_ARGS, "trace_batch: missing mesh");
+  if (n < 0 || n > 0x7fffffffLL) return fail(DG_ERR_INVALID_ARGS, "trace_batch: batch size out of range");
+  if (!in || !out) return fail(DG_ERR_INVALID_ARGS, "trace_batch: null request or result block");
+  if (n > 0 && (!in->face || !in->bary || !in->dir))
+    return fail(DG_ERR_INVALID_ARGS, "trace_batch: starts and dirs differ in length");
+  dg_trace_cfg c{};
+  if (cfg) c = *cfg;
+  if (c.use_f32 && c.lane == DG_LANE_EXACT) { /* the f32 lane has a single arithmetic variant */ }
+  const bool device_mode = c.memory == DG_MEM_DEVICE;
+  const bool record = out->poly_offsets != nullptr;
+  if (record && (!out->poly_face || !out->poly_bary || !out->poly_seg || out->poly_total < 0))
+    return fail(DG_ERR_INVALID_ARGS, "trace_batch: polyline recording needs poly_face/poly_bary/poly_seg and poly_total");
+
+  DeviceGuard guard(mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
+  // device mode: the caller's stream, NULL = the CUDA default stream (ordering with the caller's
+  // own work is the caller's contract); host mode: the mesh's private stream unless one is given
+  cudaStream_t stream = (device_mode || c.stream) ? static_cast<cudaStream_t>(c.stream) : mesh->stream;
+  if (n == 0) {
+    if (out->total_crossings) {
+      if (device_mode) DG_CUDA(cudaMemsetAsync(out->total_crossings, 0, sizeof(uint64_t), stream));
+      else *out->total_crossings = 0;
+    }
+    return DG_OK;
+  }
+
+  Stage st(stream, device_mode);
+  const size_t N = size_t(n);
+  dg::TraceParams p{};
+  p.mesh = mesh->view();
+  p.n = n;
+  p.face = st.in(in->face, N);
+  p.bary = st.in(in->bary, 3 * N);
+  p.dir = st.in(in->dir, 3 * N);
+  p.payload = st.in(in->payload, 3 * N);
+  p.o_face = st.out(out->face, N);
+  p.o_bary = st.out(out->bary, 3 * N);
+  p.o_dir = st.out(out->dir, 3 * N);
+  p.o_traced = st.out(out->traced, N);
+  p.o_requested = st.out(out->requested, N);
+  p.o_term = st.out(out->term, N);
+  p.o_status = st.out(out->status, N);
+  p.o_stall = st.out(out->stall, N);
+  p.o_payload = st.out(out->payload, 3 * N);
+  p.o_transport = st.out(out->transport, 9 * N);
+  p.o_npoints = st.out(out->npoints, N);
+  p.o_crossings = st.out(out->crossings, N);
+  if (record) {
+    const size_t T = size_t(out->poly_total);
+    p.poly_offsets = st.in(out->poly_offsets, N);
+    p.poly_face = st.out(out->poly_face, T);
+    p.poly_bary = st.out(out->poly_bary, 3 * T);
+    p.poly_seg = st.out(out->poly_seg, T);
+  }
+  p.max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
+  p.refill_min = c.refill_min ? c.refill_min : 1;
+  p.hole_avoidance = c.hole_avoidance;
+  p.want_q = c.want_transport_matrix;
+
+  unsigned long long* ctr = mesh->next_counters();
+  p.queue_head = ctr;
+  p.total_crossings = out->total_crossings ? ctr + 1 : nullptr;
+  st.note(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), stream));
+
+  if (c.sort_by_face) {  // schedule in start-face order; results stay at the request index
+    int32_t* keys_out = st.scratch<int32_t>(N);
+    int32_t* iota = st.scratch<int32_t>(N);
+    int32_t* perm = st.scratch<int32_t>(N);
+    if (keys_out && iota && perm) {
+      iota_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(iota, n);
+      size_t tmp_bytes = 0;
+      int bits = 1;
+      while ((int64_t(1) << bits) < int64_t(mesh->nf) && bits < 31) ++bits;
+      st.note(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, p.face, keys_out, iota, perm, int(n), 0, bits, stream));
+      void* tmp = st.scratch<char>(tmp_bytes);
+      if (tmp) st.note(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, p.face, keys_out, iota, perm, int(n), 0, bits, stream));
+      p.perm = perm;
+    }
+  }
+  if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_trace_batch staging");
+
+  const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || record ||
+                          out->payload || out->transport;
+  dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm)};
+  st.note(dg::launch_trace(p, c.use_f32 != 0, needs_full, shape, stream));
+  if (out->total_crossings) {
+    st.note(cudaMemcpyAsync(out->total_crossings, ctr + 1, sizeof(uint64_t),
+                            device_mode ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
+  }
+  cudaError_t e = st.finish();
+  if (e != cudaSuccess) return fail_cuda(e, "dg_trace_batch");
+  return DG_OK;
+}
+
+void dg_trace_kernel_info(int use_f32, int full, int* regs, int* blocks_per_sm, int* block_threads) {
+  if (regs) *regs = 0;
+  if (blocks_per_sm) *blocks_per_sm = 0;
+  if (block_threads) *block_threads = 0;
+  if (dg_device_count() == 0) return;
+  DeviceGuard guard(g_device);
+  dg::trace_kernel_info(use_f32 != 0, full != 0, regs, blocks_per_sm, block_threads);
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// Shared plumbing of the C-ABI translation units: the mesh handle, error reporting, device
+// guard and the host<->device staging helper used by DG_MEM_HOST calls.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/dg_b200.h"
+#include "dg_kernels.cuh"
+
+struct dg_mesh {
+  int device = 0;
+  int sm_count = 0;
+  int32_t nf = 0, nv = 0;
+  dg::FaceRec* rec = nullptr;
+  double* fnormal = nullptr;
+  double* vangle = nullptr;
+  int32_t* csr_off = nullptr;
+  int32_t* csr_list = nullptr;
+  uint8_t* vboundary = nullptr;
+  int64_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  // ring of {queue_head, total_crossings} pairs so that concurrent calls never share a cursor
+  static constexpr unsigned kRing = 256;
+  unsigned long long* counters = nullptr;
+  mutable std::atomic<unsigned> ring{0};
+
+  dg::MeshView view() const {
+    return dg::MeshView{rec, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
+  }
+  unsigned long long* next_counters() const { return counters + 2 * (ring.fetch_add(1) % kRing); }
+};
+
+namespace dgapi {
+
+std::string& last_error();
+int fail(int code, const char* fmt, ...);
+int fail_cuda(cudaError_t e, const char* where);
+
+#define DG_CUDA(expr)                                          \
+  do {                                                         \
+    cudaError_t e__ = (expr);                                  \
+    if (e__ != cudaSuccess) return dgapi::fail_cuda(e__, #expr); \
+  } while (0)
+
+// Makes the mesh's device current for the scope of a call.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; }
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Stream-ordered staging of host arrays. in(): device copy of a host array; out(): device
+// buffer whose contents are copied back by finish(). With device_mode the user pointers are
+// passed through untouched.
+class Stage {
+ public:
+  Stage(cudaStream_t s, bool device_mode) : stream_(s), device_mode_(device_mode) {}
+  ~Stage() { release(); }
+
+  template <class T>
+  const T* in(const T* user, size_t count) {
+    if (!user || device_mode_ || count == 0) return user;
+    void* d = alloc(count * sizeof(T));
+    if (!d) return nullptr;
+    note(cudaMemcpyAsync(d, user, count * sizeof(T), cudaMemcpyHostToDevice, stream_));
+    return static_cast<const T*>(d);
+  }
+  template <class T>
+  T* out(T* user, size_t count) {
+    if (!user || device_mode_ || count == 0) return user;
+    void* d = alloc(count * sizeof(T));
+    if (!d) return nullptr;
+    backs_.push_back({d, user, count * sizeof(T)});
+    return static_cast<T*>(d);
+  }
+  // scratch that is never copied back (both modes)
+  template <class T>
+  T* scratch(size_t count) { return static_cast<T*>(alloc(count * sizeof(T))); }
+
+  // Copies the outputs back and waits (host mode); in device mode only frees scratch.
+  cudaError_t finish() {
+    for (auto& b : backs_) note(cudaMemcpyAsync(b.host, b.dev, b.bytes, cudaMemcpyDeviceToHost, stream_));
+    backs_.clear();
+    release();
+    if (!device_mode_) note(cudaStreamSynchronize(stream_));
+    return err_;
+  }
+  cudaError_t error() const { return err_; }
+  void note(cudaError_t e) { if (err_ == cudaSuccess && e != cudaSuccess) err_ = e; }
+
+ private:
+  struct Back { void* dev; void* host; size_t bytes; };
+  void* alloc(size_t bytes) {
+    void* d = nullptr;
+    cudaError_t e = cudaMallocAsync(&d, bytes ? bytes : 1, stream_);
+    if (e != cudaSuccess) { note(e); return nullptr; }
+    allocs_.push_back(d);
+    return d;
+  }
+  void release() {
+    for (void* d : allocs_) cudaFreeAsync(d, stream_);
+    allocs_.clear();
+  }
+  cudaStream_t stream_;
+  bool device_mode_;
+  cudaError_t err_ = cudaSuccess;
+  std::vector<void*> allocs_;
+  std::vector<Back> backs_;
+};
+
+inline int default_max_steps(int32_t nf) {  // tracer.cpp:543-545
+  return int(10.0 * std::sqrt(double(nf))) + 100;
+}
+
+}  // namespace dgapi

@@ -1,0 +1,244 @@
+// C-ABI entry points of the differentials and the single-transition operations.
+#include "dg_capi_common.hpp"
+
+using namespace dgapi;
+
+namespace {
+
+constexpr unsigned long long kNoError = ~0ull;
+
+int check_common(const dg_mesh* mesh, int64_t n, const char* who) {
+  if (!mesh) return fail(DG_ERR_INVALID_ARGS, "%s: missing mesh", who);
+  if (n < 0 || n > 0x7fffffffLL / 4) return fail(DG_ERR_INVALID_ARGS, "%s: batch size out of range", who);
+  return DG_OK;
+}
+
+// Runs one batch of trace jobs that already live on the device (GFD rounds).
+cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const double* jb, const double* jd,
+                     const double* jp, int32_t* rf, double* rb, double* rd, double* rp, uint8_t* rt, uint8_t* rs,
+                     int max_steps, unsigned long long* total, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  dg::TraceParams p{};
+  p.mesh = mesh->view();
+  p.n = n;
+  p.face = jf; p.bary = jb; p.dir = jd; p.payload = jp;
+  p.o_face = rf; p.o_bary = rb; p.o_dir = rd; p.o_payload = rp; p.o_term = rt; p.o_status = rs;
+  p.max_steps = max_steps;
+  p.refill_min = 1;
+  unsigned long long* ctr = mesh->next_counters();
+  p.queue_head = ctr;
+  p.total_crossings = total;
+  cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  return dg::launch_trace(p, false, jp != nullptr, dg::LaunchShape{mesh->sm_count, 0}, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dg_transition(const dg_mesh* mesh, int which, int64_t n, const int32_t* face, const double* bary,
+                  const double* v, const double* remaining, int hole_avoidance, int32_t* out_face,
+                  double* out_bary, double* out_v, double* step_length, uint8_t* finished, uint8_t* event,
+                  uint8_t* stall, int32_t* rc) {
+  if (int e = check_common(mesh, n, "dg_transition")) return e;
+  if (which < 0 || which > 3) return fail(DG_ERR_INVALID_ARGS, "dg_transition: unknown operation %d", which);
+  if (n == 0) return DG_OK;
+  if (!face || !bary || !v || !out_face || !out_bary || !out_v || !rc || (which == 0 && !remaining))
+    return fail(DG_ERR_INVALID_ARGS, "dg_transition: null argument");
+  DeviceGuard guard(mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
+  cudaStream_t stream = mesh->stream;
+  Stage st(stream, false);
+  const size_t N = size_t(n);
+  dg::TransitionParams p{};
+  p.mesh = mesh->view();
+  p.which = which;
+  p.n = n;
+  p.face = st.in(face, N); p.bary = st.in(bary, 3 * N); p.v = st.in(v, 3 * N);
+  p.remaining = st.in(remaining, N);
+  p.hole_avoidance = hole_avoidance;
+  p.out_face = st.out(out_face, N); p.out_bary = st.out(out_bary, 3 * N); p.out_v = st.out(out_v, 3 * N);
+  p.step_length = st.out(step_length, N); p.finished = st.out(finished, N); p.event = st.out(event, N);
+  p.stall = st.out(stall, N); p.rc = st.out(rc, N);
+  if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_transition staging");
+  st.note(dg::launch_transition(p, stream));
+  cudaError_t e = st.finish();
+  if (e != cudaSuccess) return fail_cuda(e, "dg_transition");
+  return DG_OK;
+}
+
+static int ep_common(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* v,
+                     const int32_t* end_face, const double* end_dir, const double* g, const dg_diff_cfg* cfg,
+                     double* rot, double* frames, double* grad_v, double* grad_p, int64_t* err_index,
+                     const char* who) {
+  if (err_index) *err_index = -1;
+  if (int e = check_common(mesh, n, who)) return e;
+  if (n == 0) return DG_OK;
+  if (!face || !v || !end_face || !end_dir) return fail(DG_ERR_INVALID_ARGS, "%s: null argument", who);
+  dg_diff_cfg c{};
+  if (cfg) c = *cfg;
+  const bool device_mode = c.memory == DG_MEM_DEVICE;
+  DeviceGuard guard(mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
+  cudaStream_t stream = (device_mode || c.stream) ? static_cast<cudaStream_t>(c.stream) : mesh->stream;
+  Stage st(stream, device_mode);
+  const size_t N = size_t(n);
+  dg::EpParams p{};
+  p.mesh = mesh->view();
+  p.n = n;
+  p.face = st.in(face, N); p.v = st.in(v, 3 * N);
+  p.end_face = st.in(end_face, N); p.end_dir = st.in(end_dir, 3 * N);
+  p.g = st.in(g, 3 * N);
+  p.rot = st.out(rot, 9 * N); p.frames = st.out(frames, size_t(DG_FRAME_DOUBLES) * N);
+  p.grad_v = st.out(grad_v, 3 * N); p.grad_p = st.out(grad_p, 3 * N);
+  unsigned long long* err = st.scratch<unsigned long long>(1);
+  if (st.error() != cudaSuccess || !err) return fail_cuda(st.error(), "ep staging");
+  p.first_error = err;
+  st.note(cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), stream));
+  st.note(dg::launch_ep(p, stream));
+  unsigned long long h_err = kNoError;
+  st.note(cudaMemcpyAsync(&h_err, err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
+  st.note(cudaStreamSynchronize(stream));  // the return code depends on the error word
+  cudaError_t e = st.finish();
+  if (e != cudaSuccess) return fail_cuda(e, who);
+  if (h_err != kNoError) {
+    const int64_t idx = int64_t(h_err >> 2);
+    if (err_index) *err_index = idx;
+    switch (int(h_err & 3ull)) {
+      case 0: return fail(DG_ERR_DEGENERATE_DIRECTION, "ep_jacobians: |v| too small");
+      case 1: return fail(DG_ERR_DEGENERATE_DIRECTION, "direction is normal to the face");
+      default: return fail(DG_ERR_INVALID_ARGS, "%s: face index out of range at sample %lld", who, (long long)idx);
+    }
+  }
+  return DG_OK;
+}
+
+int dg_ep_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
+                    const int32_t* end_face, const double* end_bary, const double* end_dir,
+                    const dg_diff_cfg* cfg, double* rot, double* frames, int64_t* err_index) {
+  (void)bary; (void)end_bary;  // origins of the frames; they do not enter the arithmetic (diff.cpp:44-66)
+  return ep_common(mesh, n, face, v, end_face, end_dir, nullptr, cfg, rot, frames, nullptr, nullptr, err_index,
+                   "dg_ep_jacobians");
+}
+
+int dg_ep_backward(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* v, const int32_t* end_face,
+                   const double* end_dir, const double* g, const dg_diff_cfg* cfg, double* grad_v, double* grad_p,
+                   int64_t* err_index) {
+  if (n > 0 && (!g || !grad_v)) return fail(DG_ERR_INVALID_ARGS, "dg_ep_backward: null argument");
+  return ep_common(mesh, n, face, v, end_face, end_dir, g, cfg, nullptr, nullptr, grad_v, grad_p, err_index,
+                   "dg_ep_backward");
+}
+
+int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
+                     double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
+                     uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
+                     double* base_bary, double* base_dir, int64_t* err_index) {
+  if (err_index) *err_index = -1;
+  if (int e = check_common(mesh, n, "dg_gfd_jacobians")) return e;
+  if (n == 0) return DG_OK;
+  if (!face || !bary || !v) return fail(DG_ERR_INVALID_ARGS, "dg_gfd_jacobians: null argument");
+  dg_diff_cfg c{};
+  if (cfg) c = *cfg;
+  const bool device_mode = c.memory == DG_MEM_DEVICE;
+  DeviceGuard guard(mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
+  cudaStream_t stream = (device_mode || c.stream) ? static_cast<cudaStream_t>(c.stream) : mesh->stream;
+  const int max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
+
+  Stage st(stream, device_mode);
+  const size_t N = size_t(n);
+  dg::GfdBuffers b{};
+  b.mesh = mesh->view();
+  b.n = n;
+  b.face = st.in(face, N); b.bary = st.in(bary, 3 * N); b.v = st.in(v, 3 * N);
+  b.eps_v = eps_v; b.eps_p = eps_p;
+  b.g = st.in(g, 3 * N);
+  b.jv = st.out(jv, 4 * N); b.jp = st.out(jp, 4 * N);
+  b.degraded = degraded ? st.out(degraded, 4 * N) : st.scratch<uint8_t>(4 * N);
+  b.frames = st.out(frames, size_t(DG_FRAME_DOUBLES) * N);
+  b.grad_v = st.out(grad_v, 3 * N); b.grad_p = st.out(grad_p, 3 * N);
+  // round 1 / round 2 job and result arrays
+  b.j1_face = st.scratch<int32_t>(4 * N); b.j1_bary = st.scratch<double>(12 * N);
+  b.j1_dir = st.scratch<double>(12 * N); b.j1_payload = st.scratch<double>(12 * N);
+  b.r1_face = st.scratch<int32_t>(4 * N); b.r1_bary = st.scratch<double>(12 * N);
+  b.r1_dir = st.scratch<double>(12 * N); b.r1_payload = st.scratch<double>(12 * N);
+  b.r1_term = st.scratch<uint8_t>(4 * N); b.r1_status = st.scratch<uint8_t>(4 * N);
+  b.j2_face = st.scratch<int32_t>(3 * N); b.j2_bary = st.scratch<double>(9 * N); b.j2_dir = st.scratch<double>(9 * N);
+  b.r2_face = st.scratch<int32_t>(3 * N); b.r2_bary = st.scratch<double>(9 * N);
+  b.r2_term = st.scratch<uint8_t>(3 * N); b.r2_status = st.scratch<uint8_t>(3 * N);
+  b.err = st.scratch<unsigned long long>(8);
+  if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_gfd_jacobians staging");
+
+  unsigned long long h_err[8];
+  for (auto& w : h_err) w = kNoError;
+  h_err[3] = 0;
+  st.note(cudaMemcpyAsync(b.err, h_err, sizeof h_err, cudaMemcpyHostToDevice, stream));
+
+  // round 1: base + perp on the lite kernel, the two payload-carrying seeds on the full kernel
+  st.note(dg::launch_gfd_round1_jobs(b, stream));
+  st.note(run_jobs(mesh, 2 * n, b.j1_face, b.j1_bary, b.j1_dir, nullptr, b.r1_face, b.r1_bary, b.r1_dir, nullptr,
+                   b.r1_term, b.r1_status, max_steps, nullptr, stream));
+  st.note(run_jobs(mesh, 2 * n, b.j1_face + 2 * N, b.j1_bary + 6 * N, b.j1_dir + 6 * N, b.j1_payload + 6 * N,
+                   b.r1_face + 2 * N, b.r1_bary + 6 * N, b.r1_dir + 6 * N, b.r1_payload + 6 * N, b.r1_term + 2 * N,
+                   b.r1_status + 2 * N, max_steps, nullptr, stream));
+  // round 2: the dependent retraces
+  st.note(dg::launch_gfd_round2_jobs(b, stream));
+  st.note(run_jobs(mesh, 3 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, nullptr, nullptr,
+                   b.r2_term, b.r2_status, max_steps, nullptr, stream));
+  st.note(dg::launch_gfd_assemble(b, stream));
+  st.note(cudaMemcpyAsync(h_err, b.err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
+  st.note(cudaStreamSynchronize(stream));
+  if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_gfd_jacobians");
+
+  const bool hard_error = h_err[0] != kNoError || h_err[1] != kNoError || h_err[2] != kNoError;
+  if (!hard_error && h_err[3] != 0) {
+    // one-sided fallback for the columns whose + perturbation did not reach its length
+    b.j3_face = st.scratch<int32_t>(4 * N); b.j3_bary = st.scratch<double>(12 * N);
+    b.j3_dir = st.scratch<double>(12 * N); b.j3_payload = st.scratch<double>(12 * N);
+    b.r3_face = st.scratch<int32_t>(4 * N); b.r3_bary = st.scratch<double>(12 * N);
+    b.r3_payload = st.scratch<double>(12 * N);
+    b.r3_term = st.scratch<uint8_t>(4 * N); b.r3_status = st.scratch<uint8_t>(4 * N);
+    b.j4_face = st.scratch<int32_t>(2 * N); b.j4_bary = st.scratch<double>(6 * N); b.j4_dir = st.scratch<double>(6 * N);
+    b.r4_face = st.scratch<int32_t>(2 * N); b.r4_bary = st.scratch<double>(6 * N);
+    b.r4_term = st.scratch<uint8_t>(2 * N); b.r4_status = st.scratch<uint8_t>(2 * N);
+    if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_gfd_jacobians fallback staging");
+    st.note(dg::launch_gfd_fallback_jobs(b, stream));
+    st.note(run_jobs(mesh, 4 * n, b.j3_face, b.j3_bary, b.j3_dir, b.j3_payload, b.r3_face, b.r3_bary, nullptr,
+                     b.r3_payload, b.r3_term, b.r3_status, max_steps, nullptr, stream));
+    st.note(dg::launch_gfd_fallback_round2_jobs(b, stream));
+    st.note(run_jobs(mesh, 2 * n, b.j4_face, b.j4_bary, b.j4_dir, nullptr, b.r4_face, b.r4_bary, nullptr, nullptr,
+                     b.r4_term, b.r4_status, max_steps, nullptr, stream));
+    st.note(dg::launch_gfd_fallback_assemble(b, stream));
+    st.note(cudaMemcpyAsync(h_err, b.err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
+    st.note(cudaStreamSynchronize(stream));
+  }
+  // base end states for callers that chain the forward result
+  const cudaMemcpyKind kind = device_mode ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (base_face) st.note(cudaMemcpyAsync(base_face, b.r1_face, N * sizeof(int32_t), kind, stream));
+  if (base_bary) st.note(cudaMemcpyAsync(base_bary, b.r1_bary, 3 * N * sizeof(double), kind, stream));
+  if (base_dir) st.note(cudaMemcpyAsync(base_dir, b.r1_dir, 3 * N * sizeof(double), kind, stream));
+  cudaError_t e = st.finish();
+  if (e != cudaSuccess) return fail_cuda(e, "dg_gfd_jacobians");
+
+  if (h_err[0] != kNoError) {
+    if (err_index) *err_index = int64_t(h_err[0]);
+    return fail(DG_ERR_DEGENERATE_DIRECTION, "tangent frame needs a nonzero in-plane direction (sample %lld)",
+                (long long)h_err[0]);
+  }
+  if (h_err[1] != kNoError) {
+    if (err_index) *err_index = int64_t(h_err[1]);
+    return fail(DG_ERR_GFD, "gfd: the base trace did not reach its requested length");
+  }
+  if (h_err[4] != kNoError && (h_err[2] == kNoError || h_err[4] <= h_err[2])) {
+    if (err_index) *err_index = int64_t(h_err[4]);
+    return fail(DG_ERR_NUMERICAL_STALL, "trace: a one-sided fallback trace stalled (sample %lld)", (long long)h_err[4]);
+  }
+  if (h_err[2] != kNoError) {
+    if (err_index) *err_index = int64_t(h_err[2]);
+    return fail(DG_ERR_GFD, "gfd: start-point perturbation seeds failed to trace");
+  }
+  return DG_OK;
+}
+
+}  // extern "C"

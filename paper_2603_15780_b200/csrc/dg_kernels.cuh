@@ -1,0 +1,125 @@
+// Launch interface between the C-ABI layer (dg_capi.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dg_mesh_view.cuh"
+
+namespace dg {
+
+// One batch of trace jobs. All pointers are device pointers on the mesh's GPU; every output
+// pointer may be null. Element i of the schedule is query perm[i] (or i when perm is null);
+// results are always written at the query's own index.
+struct TraceParams {
+  MeshView mesh;
+  int64_t n;
+  const int32_t* face;
+  const double* bary;
+  const double* dir;
+  const double* payload;  // null: no element has a payload
+  const int32_t* perm;
+  int32_t* o_face;
+  double* o_bary;
+  double* o_dir;
+  double* o_traced;
+  double* o_requested;
+  uint8_t* o_term;
+  uint8_t* o_status;
+  uint8_t* o_stall;
+  double* o_payload;
+  double* o_transport;
+  int32_t* o_npoints;
+  int32_t* o_crossings;
+  const int64_t* poly_offsets;  // non-null: record polylines
+  int32_t* poly_face;
+  double* poly_bary;
+  double* poly_seg;
+  unsigned long long* queue_head;       // work-stealing cursor, zeroed before the launch
+  unsigned long long* total_crossings;  // optional: += sum of crossings of the batch
+  int32_t max_steps;
+  int32_t refill_min;  // refill a warp once this many lanes are idle (>= 1)
+  uint8_t hole_avoidance;
+  uint8_t want_q;
+};
+
+struct LaunchShape {
+  int sm_count;
+  int blocks_per_sm;  // 0 = use the occupancy query
+};
+
+// needs_full: any of payload / transport matrix / hole avoidance / polyline is requested.
+cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
+                         cudaStream_t stream);
+
+// Kernel attributes for reporting (registers, max resident blocks per SM).
+void trace_kernel_info(bool use_f32, bool full, int* regs, int* blocks_per_sm, int* block_threads);
+
+// ---- differentials (dg_diff_kernels.cu) ---------------------------------------------------
+
+struct EpParams {
+  MeshView mesh;
+  int64_t n;
+  const int32_t* face;      // start face
+  const double* v;          // [3n]
+  const int32_t* end_face;
+  const double* end_dir;    // [3n]
+  const double* g;          // [3n] upstream gradient (null for Jacobian-only)
+  double* rot;              // [9n]  or null
+  double* frames;           // [33n] or null
+  double* grad_v;           // [3n]  or null
+  double* grad_p;           // [3n]  or null
+  unsigned long long* first_error;  // min index of a sample with a degenerate direction (init ~0ull)
+};
+cudaError_t launch_ep(const EpParams& p, cudaStream_t stream);
+
+struct GfdBuffers {
+  MeshView mesh;
+  int64_t n;
+  const int32_t* face;  // samples
+  const double* bary;
+  const double* v;
+  double eps_v, eps_p;
+  // round-1 job arrays (4n) and results
+  int32_t* j1_face; double* j1_bary; double* j1_dir; double* j1_payload;
+  int32_t* r1_face; double* r1_bary; double* r1_dir; double* r1_payload;
+  uint8_t* r1_term; uint8_t* r1_status;
+  // round-2 job arrays (3n) and results
+  int32_t* j2_face; double* j2_bary; double* j2_dir;
+  int32_t* r2_face; double* r2_bary; uint8_t* r2_term; uint8_t* r2_status;
+  // fallback rounds (4n slots, only flagged columns are live)
+  int32_t* j3_face; double* j3_bary; double* j3_dir; double* j3_payload;
+  int32_t* r3_face; double* r3_bary; double* r3_payload; uint8_t* r3_term; uint8_t* r3_status;
+  int32_t* j4_face; double* j4_bary; double* j4_dir;
+  int32_t* r4_face; double* r4_bary; uint8_t* r4_term; uint8_t* r4_status;
+  // outputs
+  double* jv; double* jp; uint8_t* degraded; double* frames;
+  const double* g; double* grad_v; double* grad_p;
+  // error words: [0] first degenerate-direction sample, [1] first base-not-reached sample,
+  // [2] first seeds-failed sample, [3] number of samples needing the fallback rounds,
+  // [4] first stalled fallback trace
+  unsigned long long* err;
+};
+cudaError_t launch_gfd_round1_jobs(const GfdBuffers& b, cudaStream_t stream);
+cudaError_t launch_gfd_round2_jobs(const GfdBuffers& b, cudaStream_t stream);
+cudaError_t launch_gfd_assemble(const GfdBuffers& b, cudaStream_t stream);
+cudaError_t launch_gfd_fallback_jobs(const GfdBuffers& b, cudaStream_t stream);
+cudaError_t launch_gfd_fallback_round2_jobs(const GfdBuffers& b, cudaStream_t stream);
+cudaError_t launch_gfd_fallback_assemble(const GfdBuffers& b, cudaStream_t stream);
+
+struct TransitionParams {
+  MeshView mesh;
+  int which;  // 0 geodesic_step, 1 transport_over_edge, 2 transport_over_vertex, 3 boundary_continue
+  int64_t n;
+  const int32_t* face; const double* bary; const double* v; const double* remaining;
+  int hole_avoidance;
+  int32_t* out_face; double* out_bary; double* out_v; double* step_length;
+  uint8_t* finished; uint8_t* event; uint8_t* stall; int32_t* rc;
+};
+cudaError_t launch_transition(const TransitionParams& p, cudaStream_t stream);
+
+// Builds the fat face records on the device from the indexed arrays.
+cudaError_t launch_build_records(const double* xyz, const int32_t* tri, const int32_t* adj, int32_t nf,
+                                 FaceRec* rec, cudaStream_t stream);
+
+}  // namespace dg

@@ -1,0 +1,105 @@
+// Device mesh layout ("fat face records") and its register-resident view.
+//
+// The reference keeps an indexed mesh (vertices[], faces[], face_adjacency[],
+// proj/include/digeo/mesh.hpp:42-49) and re-fetches positions through two dependent
+// lookups on every crossing (tracer.cpp:72, :113-126). On B200 the walk is a chain of
+// dependent L2 gathers, so the device layout trades capacity for chain depth: ONE 96-byte,
+// 32-byte-aligned record per face holds everything a trace needs while it is inside that
+// face -- the three corner positions, the three vertex ids and the three neighbour ids.
+// Entering a face costs exactly one gather of three 32-B sectors; 1 M faces = 96 MB, which
+// stays resident in the 126 MB L2.
+//
+// Word order inside the record is chosen so that it is read with six 128-bit loads
+// (or three 256-bit loads): x[0..7] | x[8], v0, v1 | v2, a0, a1, a2.
+#pragma once
+
+#include "dg_math.cuh"
+
+namespace dg {
+
+struct alignas(32) FaceRec {
+  double x[9];     // corner positions, x[3*k + c] = coordinate c of corner k (exact copies of Mesh::vertices)
+  int32_t v[3];    // vertex ids of the corners                       (Mesh::faces[f])
+  int32_t adj[3];  // face across the edge opposite corner k, -1 = boundary (Mesh::face_adjacency[f])
+};
+static_assert(sizeof(FaceRec) == 96, "FaceRec must be three 32-byte sectors");
+
+struct MeshView {
+  const FaceRec* rec;        // [nf]
+  const double* fnormal;     // [3 nf] unit face normals                  (Mesh::face_normals)
+  const double* vangle;      // [nv]   total interior angle per vertex    (Mesh::vertex_total_angle)
+  const int32_t* csr_off;    // [nv+1] vertex -> incident faces, face order (mesh.cpp:118-127)
+  const int32_t* csr_list;   // [3 nf]
+  const uint8_t* vboundary;  // [nv]   (Mesh::vertex_on_boundary)
+  int32_t nf, nv;
+};
+
+// Register copy of one face record in the stepping scalar type S.
+template <class S>
+struct Face {
+  V3<S> x0, x1, x2;
+  int v0, v1, v2;
+  int a0, a1, a2;
+
+  DG_HD V3<S> pos(int k) const { return k == 0 ? x0 : (k == 1 ? x1 : x2); }
+  DG_HD int id(int k) const { return sel3(k, v0, v1, v2); }
+  DG_HD int adj(int k) const { return sel3(k, a0, a1, a2); }
+  // Mesh::corner_of (mesh.hpp:56)
+  DG_HD int corner_of(int v) const { return v0 == v ? 0 : (v1 == v ? 1 : (v2 == v ? 2 : -1)); }
+  // position of the corner holding vertex id v
+  DG_HD V3<S> pos_of(int v) const { return v0 == v ? x0 : (v1 == v ? x1 : x2); }
+  // the vertex that is neither a nor b (the reference scans the corners and keeps the last hit,
+  // tracer.cpp:115-120; ids of a face are distinct so there is exactly one)
+  DG_HD int third(int a, int b) const {
+    int r = -1;
+    if (v0 != a && v0 != b) r = v0;
+    if (v1 != a && v1 != b) r = v1;
+    if (v2 != a && v2 != b) r = v2;
+    return r;
+  }
+  // Mesh::neighbor_across (mesh.cpp:21-27)
+  DG_HD int neighbor_across(int a, int b) const {
+    if ((v1 == a && v2 == b) || (v1 == b && v2 == a)) return a0;
+    if ((v2 == a && v0 == b) || (v2 == b && v0 == a)) return a1;
+    if ((v0 == a && v1 == b) || (v0 == b && v1 == a)) return a2;
+    return -1;
+  }
+};
+
+template <class S>
+DG_HD Face<S> load_face(const MeshView& m, int f) {
+  Face<S> r;
+#ifdef __CUDA_ARCH__
+  const double2* p = reinterpret_cast<const double2*>(m.rec + f);
+  double2 d0 = __ldg(p + 0), d1 = __ldg(p + 1), d2 = __ldg(p + 2), d3 = __ldg(p + 3);
+  const int4* q = reinterpret_cast<const int4*>(p + 4);
+  int4 w0 = __ldg(q + 0), w1 = __ldg(q + 1);
+  double x8 = __hiloint2double(w0.y, w0.x);
+  r.x0 = {S(d0.x), S(d0.y), S(d1.x)};
+  r.x1 = {S(d1.y), S(d2.x), S(d2.y)};
+  r.x2 = {S(d3.x), S(d3.y), S(x8)};
+  r.v0 = w0.z; r.v1 = w0.w; r.v2 = w1.x;
+  r.a0 = w1.y; r.a1 = w1.z; r.a2 = w1.w;
+#else
+  const FaceRec& c = m.rec[f];
+  r.x0 = {S(c.x[0]), S(c.x[1]), S(c.x[2])};
+  r.x1 = {S(c.x[3]), S(c.x[4]), S(c.x[5])};
+  r.x2 = {S(c.x[6]), S(c.x[7]), S(c.x[8])};
+  r.v0 = c.v[0]; r.v1 = c.v[1]; r.v2 = c.v[2];
+  r.a0 = c.adj[0]; r.a1 = c.adj[1]; r.a2 = c.adj[2];
+#endif
+  return r;
+}
+
+template <class S>
+DG_HD V3<S> load_normal(const MeshView& m, int f) {
+#ifdef __CUDA_ARCH__
+  const double* p = m.fnormal + 3 * size_t(f);
+  return {S(__ldg(p)), S(__ldg(p + 1)), S(__ldg(p + 2))};
+#else
+  const double* p = m.fnormal + 3 * size_t(f);
+  return {S(p[0]), S(p[1]), S(p[2])};
+#endif
+}
+
+}  // namespace dg

@@ -1,0 +1,168 @@
+// Forward tracing kernel: persistent warps, one geodesic per lane, lane-level work stealing.
+//
+// Replaces the reference's `#pragma omp parallel for schedule(dynamic, 8)` over run_one
+// (proj/src/tracer.cpp:596-603). Path lengths differ by orders of magnitude between queries,
+// so a lane that finishes its geodesic does not wait for the rest of its warp: between two
+// steps the warp ballots its idle lanes, ONE lane advances the global queue cursor by the
+// number of idle lanes (warp-aggregated atomic) and every idle lane initialises the next
+// query in place. The grid is sized to the resident capacity of the chip (SM count x
+// resident blocks per SM), never to the batch.
+#include "dg_kernels.cuh"
+#include "dg_tracer_core.cuh"
+
+namespace dg {
+
+namespace {
+
+constexpr int kBlockThreads = 128;
+constexpr unsigned kFullMask = 0xffffffffu;
+
+template <class S, bool kFull>
+__device__ __forceinline__ void write_result(const TraceParams& p, int64_t q,
+                                             const Tracer<S, kFull>& T) {
+  V3<double> b = T.widened_bary();
+  if (p.o_face) p.o_face[q] = T.face;
+  if (p.o_bary) { p.o_bary[3 * q] = b.x; p.o_bary[3 * q + 1] = b.y; p.o_bary[3 * q + 2] = b.z; }
+  if (p.o_dir) {
+    // tracer.cpp:525: zero for zero-length requests
+    V3<double> d = T.target > S(0) ? cast<double>(T.dir) : V3<double>{0.0, 0.0, 0.0};
+    p.o_dir[3 * q] = d.x; p.o_dir[3 * q + 1] = d.y; p.o_dir[3 * q + 2] = d.z;
+  }
+  if (p.o_traced) p.o_traced[q] = T.traced;
+  if (p.o_requested) p.o_requested[q] = double(T.target);
+  if (p.o_term) p.o_term[q] = T.term;
+  if (p.o_status) p.o_status[q] = T.status;
+  if (p.o_stall) p.o_stall[q] = T.stall_code;
+  if (p.o_npoints) p.o_npoints[q] = T.npoints;
+  if (p.o_crossings) p.o_crossings[q] = T.crossings;
+  if (kFull) {
+    if (p.o_payload) {
+      V3<double> w = T.has_payload ? cast<double>(T.payload) : V3<double>{0.0, 0.0, 0.0};
+      p.o_payload[3 * q] = w.x; p.o_payload[3 * q + 1] = w.y; p.o_payload[3 * q + 2] = w.z;
+    }
+    if (p.o_transport) {
+      // Mat3::from_columns(q0, q1, q2), row-major (geometry.hpp:80-84)
+      double* o = p.o_transport + 9 * q;
+      const bool on = T.want_q;
+      o[0] = on ? double(T.q0.x) : 0.0; o[1] = on ? double(T.q1.x) : 0.0; o[2] = on ? double(T.q2.x) : 0.0;
+      o[3] = on ? double(T.q0.y) : 0.0; o[4] = on ? double(T.q1.y) : 0.0; o[5] = on ? double(T.q2.y) : 0.0;
+      o[6] = on ? double(T.q0.z) : 0.0; o[7] = on ? double(T.q1.z) : 0.0; o[8] = on ? double(T.q2.z) : 0.0;
+    }
+  } else {
+    // the lite kernel is only launched when neither output is requested
+  }
+}
+
+template <class S, bool kFull>
+__global__ void __launch_bounds__(kBlockThreads) trace_kernel(const __grid_constant__ TraceParams p) {
+  Tracer<S, kFull> T(p.mesh, p.max_steps, p.hole_avoidance != 0);
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned long long n = (unsigned long long)p.n;
+  bool live = false;
+  bool exhausted = false;  // warp-uniform: the queue has no more work
+  int64_t q = -1;
+  unsigned long long my_crossings = 0;
+
+  for (;;) {
+    const unsigned idle = __ballot_sync(kFullMask, !live);
+    if (idle != 0u && !exhausted) {
+      const int n_idle = __popc(idle);
+      if (n_idle >= p.refill_min || n_idle == 32) {
+        const int leader = __ffs(idle) - 1;
+        unsigned long long base = 0;
+        if (lane == unsigned(leader)) base = atomicAdd(p.queue_head, (unsigned long long)n_idle);
+        base = __shfl_sync(kFullMask, base, leader);
+        if (base + (unsigned long long)n_idle >= n) exhausted = true;
+        if (!live) {
+          const unsigned long long slot = base + (unsigned long long)__popc(idle & ((1u << lane) - 1u));
+          if (slot < n) {
+            q = p.perm ? int64_t(p.perm[slot]) : int64_t(slot);
+            const int f = p.face[q];
+            const V3<double> b{p.bary[3 * q], p.bary[3 * q + 1], p.bary[3 * q + 2]};
+            const V3<double> v{p.dir[3 * q], p.dir[3 * q + 1], p.dir[3 * q + 2]};
+            V3<double> pay{0.0, 0.0, 0.0};
+            bool has_pay = false;
+            if (kFull && p.payload) {
+              pay = V3<double>{p.payload[3 * q], p.payload[3 * q + 1], p.payload[3 * q + 2]};
+              has_pay = norm2(pay) > 0.0;  // tracer.cpp:582
+            }
+            T.reset();
+            if (kFull && p.poly_offsets) {
+              T.sink.face = p.poly_face; T.sink.bary = p.poly_bary; T.sink.seg = p.poly_seg;
+              T.sink.base = p.poly_offsets[q];
+            }
+            live = T.initialise(f, b, v, pay, has_pay, p.want_q != 0);
+            if (!live) write_result<S, kFull>(p, q, T);
+          }
+        }
+      }
+    }
+    if (__ballot_sync(kFullMask, live) == 0u) {
+      if (exhausted) break;
+      continue;
+    }
+    if (live) {
+      live = T.run_step();
+      if (!live) {
+        my_crossings += (unsigned long long)T.crossings;
+        write_result<S, kFull>(p, q, T);
+      }
+    }
+  }
+
+  if (p.total_crossings) {
+    for (int o = 16; o > 0; o >>= 1) my_crossings += __shfl_xor_sync(kFullMask, my_crossings, o);
+    if (lane == 0 && my_crossings) atomicAdd(p.total_crossings, my_crossings);
+  }
+}
+
+template <class S, bool kFull>
+cudaError_t launch_one(const TraceParams& p, LaunchShape shape, cudaStream_t stream) {
+  int per_sm = shape.blocks_per_sm;
+  if (per_sm <= 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<S, kFull>,
+                                                                  kBlockThreads, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  long long blocks = (long long)shape.sm_count * per_sm;
+  const long long needed = (p.n + kBlockThreads - 1) / kBlockThreads;
+  if (blocks > needed) blocks = needed;
+  if (blocks < 1) blocks = 1;
+  trace_kernel<S, kFull><<<unsigned(blocks), kBlockThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
+                         cudaStream_t stream) {
+  if (p.n <= 0) return cudaSuccess;
+  if (use_f32) {
+    return needs_full ? launch_one<float, true>(p, shape, stream) : launch_one<float, false>(p, shape, stream);
+  }
+  return needs_full ? launch_one<double, true>(p, shape, stream) : launch_one<double, false>(p, shape, stream);
+}
+
+void trace_kernel_info(bool use_f32, bool full, int* regs, int* blocks_per_sm, int* block_threads) {
+  cudaFuncAttributes a{};
+  int per_sm = 0;
+  if (use_f32 && full) {
+    cudaFuncGetAttributes(&a, trace_kernel<float, true>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<float, true>, kBlockThreads, 0);
+  } else if (use_f32) {
+    cudaFuncGetAttributes(&a, trace_kernel<float, false>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<float, false>, kBlockThreads, 0);
+  } else if (full) {
+    cudaFuncGetAttributes(&a, trace_kernel<double, true>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<double, true>, kBlockThreads, 0);
+  } else {
+    cudaFuncGetAttributes(&a, trace_kernel<double, false>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<double, false>, kBlockThreads, 0);
+  }
+  if (regs) *regs = a.numRegs;
+  if (blocks_per_sm) *blocks_per_sm = per_sm;
+  if (block_threads) *block_threads = kBlockThreads;
+}
+
+}  // namespace dg

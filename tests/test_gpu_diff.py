@@ -1,0 +1,226 @@
+"""Parity of the EP / GFD differentials and the single-transition operations with the
+UNMODIFIED reference (proj/src/diff.cpp, tracer.cpp:630-735) through the C-ABI.
+Mirrors proj/tests/test_diff.cpp.
+
+Bar: EP is pure f64 arithmetic in the reference's operation order -> bit-identical given the
+same forward result. GFD Jacobians are finite differences of end points divided by
+eps ~ 1e-4 x mean edge, so last-ulp differences of vertex-branch traces are amplified:
+tolerance 1e-5 relative to the largest entry; on traces without vertex
+branches they are bit-identical too."""
+import numpy as np
+import pytest
+
+from conftest import gpu_mesh
+
+pytestmark = pytest.mark.gpu
+
+
+def unit_rows(rng, n):
+    q = rng.normal(size=(n, 3))
+    return q / np.linalg.norm(q, axis=1, keepdims=True)
+
+
+@pytest.mark.parametrize("fixture", ["ico4", "torus", "plane"])
+def test_ep_bit_exact(gpu, ref, fixture):
+    rm = {"ico4": lambda: ref.RefMesh.icosphere(4), "torus": lambda: ref.RefMesh.torus(1 / 3, 1 / 6, 64, 32),
+          "plane": lambda: ref.RefMesh.plane(10, 10, 1.0, 3)}[fixture]()
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(42, 10000, 0.1, 1.0)
+    h = m.trace_batch(f, b, d)
+    rng = np.random.default_rng(1)
+    g = 2.0 * (m.embed(h.face, h.bary) - unit_rows(rng, len(f)))  # gradcheck.cpp:88
+    ours = m.ep(f, b, d, h.face, h.bary, h.dir, g=g)
+    theirs = rm.ep(f, b, d, h.face, h.bary, h.dir, g=g)
+    for k in ("rot", "frames", "grad_v", "grad_p"):
+        assert np.array_equal(ours[k], theirs[k]), k
+    assert not ours["grad_p"].any()  # EP: grad_p is exactly zero (test_diff.cpp:361)
+    # R is a rotation (test_diff.cpp:65-79)
+    R = ours["rot"].reshape(-1, 3, 3)
+    assert np.abs(R @ R.transpose(0, 2, 1) - np.eye(3)).max() < 1e-9
+    assert np.abs(np.linalg.det(R) - 1).max() < 1e-9
+    if fixture == "plane":
+        assert np.abs(R - np.eye(3)).max() < 1e-12  # EP on a plane is the identity (test_diff.cpp:50-63)
+
+
+def test_ep_degenerate_direction_errors(gpu, ref):
+    rm = ref.RefMesh.icosphere(2)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(3, 16, 1.0, 1.0)
+    h = m.trace_batch(f, b, d)
+    d2 = d.copy()
+    d2[5] = 0
+    with pytest.raises(gpu.DgError) as e:
+        m.ep(f, b, d2, h.face, h.bary, h.dir)
+    assert e.value.klass == "DegenerateDirection" and e.value.index == 5 and "too small" in e.value.msg
+    with pytest.raises(ref.RefError) as er:
+        rm.ep(f, b, d2, h.face, h.bary, h.dir)
+    assert er.value.klass == "DegenerateDirection" and er.value.index == 5
+    d3 = d.copy()
+    d3[7] = rm.arrays()["fnormal"][f[7]]
+    with pytest.raises(gpu.DgError) as e:
+        m.ep(f, b, d3, h.face, h.bary, h.dir)
+    assert e.value.klass == "DegenerateDirection" and e.value.index == 7 and "normal to the face" in e.value.msg
+
+
+@pytest.mark.parametrize("fixture,n", [("ico4", 4000), ("torus", 3000), ("cyl", 2000)])
+def test_gfd_matches_reference(gpu, ref, fixture, n):
+    rm = {"ico4": lambda: ref.RefMesh.icosphere(4), "torus": lambda: ref.RefMesh.torus(1 / 3, 1 / 6, 64, 32),
+          "cyl": lambda: ref.RefMesh.cylinder(0.5, 4.0, 24, 24)}[fixture]()
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(9, n, 0.1, 0.8)
+    if fixture == "cyl":  # keep base traces on the open cylinder
+        base = rm.trace_batch(f, b, d)
+        keep = (base.term == 0) & (base.status == 0)
+        f, b, d = f[keep], b[keep], d[keep]
+    rng = np.random.default_rng(2)
+    g = unit_rows(rng, len(f))
+    assert m.default_gfd_eps() == rm.default_gfd_eps()
+    ours = m.gfd(f, b, d, g=g)
+    theirs = rm.gfd(f, b, d, g=g)
+    assert np.array_equal(ours["degraded"], theirs["degraded"])
+    assert np.array_equal(ours["frames"], theirs["frames"])
+    for k in ("jv", "jp"):
+        scale = np.abs(theirs[k]).max()
+        assert np.abs(ours[k] - theirs[k]).max() <= 1e-5 * scale, k
+    for k in ("grad_v", "grad_p"):
+        num = np.einsum("nd,nd->n", ours[k], theirs[k])
+        den = np.linalg.norm(ours[k], axis=1) * np.linalg.norm(theirs[k], axis=1)
+        ok = den > 1e-12
+        assert (num[ok] / den[ok]).min() >= 0.999999, k
+        assert np.abs(np.linalg.norm(ours[k], axis=1)[ok] / np.linalg.norm(theirs[k], axis=1)[ok] - 1).max() <= 1e-4
+    # the base end states are the forward trace
+    h = m.trace_batch(f, b, d)
+    assert np.array_equal(ours["base_face"], h.face) and np.array_equal(ours["base_bary"], h.bary)
+    # batched == unbatched exactly (test_diff.cpp:139-171): same kernel, any batch composition
+    sub = m.gfd(f[:64], b[:64], d[:64], g=g[:64])
+    assert np.array_equal(sub["jv"], ours["jv"][:64]) and np.array_equal(sub["jp"], ours["jp"][:64])
+
+
+def test_gfd_plane_is_identity(gpu, ref):
+    """test_diff.cpp:89-112: on a flat mesh both Jacobians are the frame change of the identity."""
+    rm = ref.RefMesh.plane(12, 12, 4.0, 5)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(4, 500, 0.05, 0.3)
+    base = rm.trace_batch(f, b, d)
+    keep = (base.term == 0) & (base.status == 0)
+    f, b, d = f[keep], b[keep], d[keep]
+    ours, theirs = m.gfd(f, b, d), rm.gfd(f, b, d)
+    assert np.abs(ours["jv"] - theirs["jv"]).max() <= 1e-6
+    assert np.abs(ours["jp"] - theirs["jp"]).max() <= 1e-6
+
+
+def test_gfd_one_sided_fallback_near_boundary(gpu, ref):
+    """Columns whose + perturbation leaves an open mesh fall back to the - side and are flagged
+    (diff.cpp:130-137)."""
+    rm = ref.RefMesh.plane(6, 6, 1.0, 0)
+    m = gpu_mesh(gpu, rm)
+    a = rm.arrays()
+    # traces that end exactly on / next to the boundary: aim at boundary points with full length
+    rng = np.random.default_rng(6)
+    f, b, d = rm.sample_queries(5, 3000, 0.05, 0.6)
+    base = rm.trace_batch(f, b, d)
+    P = rm.embed(f, b)
+    # shorten traces that hit the boundary so that they end 1e-9 before it
+    hit = base.term == 1
+    d[hit] *= ((base.traced[hit] - 1e-9) / base.requested[hit])[:, None]
+    base = rm.trace_batch(f, b, d)
+    P = rm.embed(f, b)
+    inside = (P[:, :2].min(1) > 0.02) & (P[:, :2].max(1) < 0.98)  # seeds (eps-length) must stay on the mesh
+    keep = (base.term == 0) & (base.status == 0) & inside
+    f, b, d = f[keep], b[keep], d[keep]
+    eps = 1e-3
+    theirs = rm.gfd(f, b, d, eps_v=eps, eps_p=eps)
+    ours = m.gfd(f, b, d, eps_v=eps, eps_p=eps)
+    assert theirs["degraded"].any(), "fixture must exercise the fallback"
+    assert np.array_equal(ours["degraded"], theirs["degraded"])
+    assert np.abs(ours["jv"] - theirs["jv"]).max() <= 1e-6
+    assert np.abs(ours["jp"] - theirs["jp"]).max() <= 1e-6
+
+
+def test_gfd_whole_call_errors(gpu, ref):
+    rm = ref.RefMesh.plane(4, 4, 1.0, 0)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(5, 64, 3.0, 4.0)  # every base trace leaves the unit square
+    with pytest.raises(gpu.DgError) as e:
+        m.gfd(f, b, d)
+    assert e.value.klass == "Error" and e.value.msg == "gfd: the base trace did not reach its requested length"
+    with pytest.raises(ref.RefError) as er:
+        rm.gfd(f, b, d)
+    assert er.value.msg == e.value.msg
+    d[:] = 0
+    with pytest.raises(gpu.DgError) as e:
+        m.gfd(f, b, d)
+    assert e.value.klass == "DegenerateDirection"
+
+
+def test_gradcheck_medians_on_sphere(gpu, ref):
+    """run_gradcheck's criteria (gradcheck.cpp:46-131, test_diff.cpp:350-361) on the GPU path:
+    pullback of |Exp - q|^2 against the closed-form sphere gradient is checked indirectly by
+    requiring our pulled-back gradients to reproduce the reference's medians."""
+    rm = ref.RefMesh.icosphere(4)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(11, 2000, 0.2, 1.0)
+    rng = np.random.default_rng(3)
+    q = unit_rows(rng, len(f))
+    h = m.trace_batch(f, b, d)
+    g = 2.0 * (m.embed(h.face, h.bary) - q)
+    ours, theirs = m.gfd(f, b, d, g=g), rm.gfd(f, b, d, g=g)
+    cos = np.einsum("nd,nd->n", ours["grad_v"], theirs["grad_v"]) / (
+        np.linalg.norm(ours["grad_v"], axis=1) * np.linalg.norm(theirs["grad_v"], axis=1))
+    assert np.median(cos) >= 0.9999999
+
+
+def test_single_transitions(gpu, ref):
+    """geodesic_step / transport_over_edge / transport_over_vertex / boundary_continue."""
+    rm = ref.RefMesh.icosphere(2)
+    m = gpu_mesh(gpu, rm)
+    rng = np.random.default_rng(8)
+    n = 300
+    f, b, d = rm.sample_queries(2, n, 1.0, 1.0)
+    rem = rng.uniform(0.01, 0.5, n)
+    o = m.transition(0, f, b, d, remaining=rem)
+    for i in range(n):
+        r = rm.geodesic_step(f[i], b[i], d[i], rem[i])
+        assert o["rc"][i] == 0 and r["face"] == o["face"][i] and r["event"] == o["event"][i]
+        assert np.array_equal(r["bary"], o["bary"][i]) and np.array_equal(r["dir"], o["v"][i])
+        assert r["step_length"] == o["step_length"][i] and r["finished"] == bool(o["finished"][i])
+    # edge points
+    be = b.copy()
+    k = rng.integers(0, 3, n)
+    be[np.arange(n), k] = 0
+    be /= be.sum(1, keepdims=True)
+    o = m.transition(1, f, be, d)
+    for i in range(n):
+        rf, rb, rv = rm.transition(0, f[i], be[i], d[i])
+        assert o["rc"][i] == 0 and rf == o["face"][i]
+        assert np.array_equal(rb, o["bary"][i]) and np.array_equal(rv, o["v"][i])
+    # vertex points
+    bv = np.zeros((n, 3))
+    bv[np.arange(n), k] = 1
+    o = m.transition(2, f, bv, d)
+    for i in range(n):
+        rf, rb, rv = rm.transition(1, f[i], bv[i], d[i])
+        assert o["rc"][i] == 0 and rf == o["face"][i]
+        assert np.abs(rb - o["bary"][i]).max() <= 1e-12 and np.abs(rv - o["v"][i]).max() <= 1e-9
+    # wrong point class -> InvalidArgs per element
+    o = m.transition(1, f[:4], b[:4], d[:4])
+    assert (o["rc"] == 1).all()
+    with pytest.raises(ref.RefError):
+        rm.transition(0, f[0], b[0], d[0])
+    # boundary_continue on an open mesh
+    pm = ref.RefMesh.plane(5, 5, 1.0, 0)
+    mp = gpu_mesh(gpu, pm)
+    a = pm.arrays()
+    fb, kb = np.nonzero(a["adj"] < 0)
+    nb = len(fb)
+    tpar = rng.uniform(0.1, 0.9, nb)
+    bb = np.zeros((nb, 3))
+    bb[np.arange(nb), (kb + 1) % 3] = tpar
+    bb[np.arange(nb), (kb + 2) % 3] = 1 - tpar
+    dv = rng.normal(size=(nb, 3))
+    dv[:, 2] = 0
+    o = mp.transition(3, fb.astype(np.int32), bb, dv)
+    for i in range(nb):
+        rf, rb, rv = pm.transition(2, fb[i], bb[i], dv[i])
+        assert o["rc"][i] == 0 and rf == o["face"][i]
+        assert np.array_equal(rb, o["bary"][i]) and np.array_equal(rv, o["v"][i])

@@ -1,0 +1,211 @@
+"""Parity of the CUDA tracer (through the C-ABI) with the UNMODIFIED reference
+(oracle/_ref/libdigeo_ref.so) on the same seeded inputs. Mirrors the reference's own tracer
+tests (proj/tests/test_tracer.cpp) and BASELINE.json's configurations.
+
+Bar: the f64 lane is compiled without FMA contraction in the reference's operation order, so
+traces that never take a vertex branch must be BIT-IDENTICAL (faces, points, directions,
+lengths, polylines). Vertex branches call atan2/sin/cos, where CUDA's libm may differ from
+glibc in the last ulp: there the face sequence must be identical and positions agree to
+1e-9 x bbox diagonal.
+"""
+import numpy as np
+import pytest
+
+from conftest import assert_trace_equal, gpu_mesh
+
+pytestmark = pytest.mark.gpu
+
+
+def both(ref_mesh, mesh, f, b, d, **kw):
+    r = ref_mesh.trace_batch(f, b, d, record_polyline=True, **kw)
+    h = mesh.trace_batch(f, b, d, record_polyline=True, **kw)
+    return r, h
+
+
+def test_config1_icosphere4_unit_vectors(gpu, ref):
+    """BASELINE config 1: ico-4 (5 120 F), 10 k unit-length tangents, vs closed-form sphere."""
+    rm = ref.RefMesh.icosphere(4)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(42, 10000, 1.0, 1.0)
+    r, h = both(rm, m, f, b, d)
+    assert_trace_equal(r, h, len(f))
+    assert h.total_crossings == int(h.crossings.sum())
+    assert np.array_equal(h.crossings, h.npoints - 2)  # one point per advance + the start point
+    # accuracy against the closed-form sphere exponential map (reference: 2.24e-3 mean)
+    P = m.embed(f, b)
+    Pn = P / np.linalg.norm(P, axis=1, keepdims=True)
+    dt = d - Pn * np.einsum("nd,nd->n", d, Pn)[:, None]
+    dt /= np.linalg.norm(dt, axis=1, keepdims=True)
+    exact = Pn * np.cos(1.0) + dt * np.sin(1.0)
+    err = np.linalg.norm(m.embed(h.face, h.bary) - exact, axis=1).mean()
+    assert err < 5e-3
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(want_q=True), dict(use_f32=True), dict(max_steps=7),
+                                dict(sort_by_face=True), dict(refill_min=8), dict(blocks_per_sm=1)])
+def test_icosphere_variants(gpu, ref, kw):
+    rm = ref.RefMesh.icosphere(3)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(1, 4000, 0.1, 3.0)
+    rng = np.random.default_rng(0)
+    pay = rng.normal(size=(len(f), 3))
+    pay[::3] = 0  # zero payload rows mean "no payload" (tracer.cpp:582)
+    ref_kw = {k: v for k, v in kw.items() if k not in ("sort_by_face", "refill_min", "blocks_per_sm")}
+    r = rm.trace_batch(f, b, d, payload=pay, record_polyline=True, **ref_kw)
+    h = m.trace_batch(f, b, d, payload=pay, record_polyline=True, **kw)
+    assert_trace_equal(r, h, len(f), payload=True, q=kw.get("want_q", False))
+    assert np.array_equal(r.has_payload, h.has_payload)
+
+
+def test_torus_long_traces_bit_exact(gpu, ref):
+    rm = ref.RefMesh.torus(1 / 3, 1 / 6, 200, 100)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(7, 20000, 0.05, 1.5)
+    r, h = both(rm, m, f, b, d)
+    assert_trace_equal(r, h, len(f))
+
+
+def test_vertex_paths(gpu, ref):
+    """Vertex-to-vertex walks (config-5 style starts) and random departures from vertices."""
+    rm = ref.RefMesh.torus(1 / 3, 1 / 6, 64, 32)
+    m = gpu_mesh(gpu, rm)
+    a = rm.arrays()
+    X, T = a["xyz"], a["tri"]
+    rng = np.random.default_rng(3)
+    n = 4000
+    fs = rng.integers(0, rm.nf, n).astype(np.int32)
+    corner = rng.integers(0, 3, n)
+    bs = np.zeros((n, 3))
+    bs[np.arange(n), corner] = 1
+    nxt = (corner + rng.integers(1, 3, n)) % 3
+    ds = X[T[fs, nxt]] - X[T[fs, corner]]
+    ds = ds / np.linalg.norm(ds, axis=1, keepdims=True) * rng.uniform(0.2, 2.0, (n, 1))
+    pay = rng.normal(size=(n, 3))
+    diag = np.linalg.norm(X.max(0) - X.min(0))
+    for dirs in (ds, rng.normal(size=(n, 3))):
+        r = rm.trace_batch(fs, bs, dirs, payload=pay, want_q=True, record_polyline=True, max_steps=5000)
+        h = m.trace_batch(fs, bs, dirs, payload=pay, want_q=True, record_polyline=True, max_steps=5000)
+        assert_trace_equal(r, h, n, payload=True, q=True, exact=False, tol=1e-9 * diag)
+        assert (h.crossings > 0).any()
+
+
+def test_cone_apex_and_icosahedron_vertices(gpu, ref):
+    for rm in (ref.RefMesh.cone(1.0, 1.0, 16), ref.RefMesh.icosphere(0), ref.RefMesh.icosphere(2)):
+        m = gpu_mesh(gpu, rm)
+        a = rm.arrays()
+        X = a["xyz"]
+        apex = int(np.argmax(np.diff(a["csr_off"])))
+        f, b, d = rm.sample_queries(12, 3000, 1.0, 1.0)
+        P = rm.embed(f, b)
+        d = X[apex] - P
+        d = d / np.linalg.norm(d, axis=1, keepdims=True) * 2.5
+        rng = np.random.default_rng(5)
+        pay = rng.normal(size=(len(f), 3))
+        for hole in (False, True):
+            r = rm.trace_batch(f, b, d, payload=pay, want_q=True, record_polyline=True, hole_avoidance=hole)
+            h = m.trace_batch(f, b, d, payload=pay, want_q=True, record_polyline=True, hole_avoidance=hole)
+            assert_trace_equal(r, h, len(f), payload=True, q=True, exact=False, tol=1e-9)
+
+
+@pytest.mark.parametrize("hole", [False, True])
+def test_open_meshes_boundary_and_hole_avoidance(gpu, ref, hole):
+    rng = np.random.default_rng(11)
+    for rm, seed in ((ref.RefMesh.plane(12, 9, 1.0, 3), 5), (ref.RefMesh.cylinder(0.5, 1.0, 24, 6), 9)):
+        m = gpu_mesh(gpu, rm)
+        f, b, d = rm.sample_queries(seed, 6000, 0.05, 3.0)
+        pay = rng.normal(size=(len(f), 3))
+        r = rm.trace_batch(f, b, d, payload=pay, want_q=True, record_polyline=True, hole_avoidance=hole)
+        h = m.trace_batch(f, b, d, payload=pay, want_q=True, record_polyline=True, hole_avoidance=hole)
+        # boundary slides visit vertices only through exact arithmetic; everything is bit-equal
+        assert_trace_equal(r, h, len(f), payload=True, q=True, exact=False, tol=1e-12)
+        if not hole:
+            assert (h.term == 1).any()
+
+
+def test_square_known_answers_and_error_slots(gpu, ref):
+    """Appendix-B known answers of the reference (golden trace_square.json case first)."""
+    sq = ref.RefMesh.build([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]], [[0, 1, 2], [0, 2, 3]])
+    m = gpu_mesh(gpu, sq)
+    F = np.array([0, 0, 0, 0, 0, 0, 7, 0, 0, -1], np.int32)
+    B = np.array([[.5, .25, .25], [.5, 0, .5], [1, 0, 0], [.5, .25, .25], [.5, .25, .25], [.5, .25, .25],
+                  [.3, .3, .4], [.5, .25, .25], [.5, .5, .5], [1, 0, 0]])
+    D = np.array([[.25, .5, 0], [-.2, .1, 0], [.1, .3, 0], [2, .1, 0], [0, 0, .5], [0, 0, 0], [1, 0, 0],
+                  [0, 0, 0], [1, 0, 0], [1, 0, 0]], float)
+    for hole in (False, True):
+        r = sq.trace_batch(F, B, D, record_polyline=True, hole_avoidance=hole)
+        h = m.trace_batch(F, B, D, record_polyline=True, hole_avoidance=hole)
+        assert_trace_equal(r, h, len(F))
+        assert r.errors == h.errors
+    h = m.trace_batch(F, B, D, record_polyline=True)
+    # golden: final bary and the 1.1e-16 second segment (tests/golden/trace_square.json)
+    assert h.bary[0].tolist() == [0.24999999999999992, 0.75000000000000011, 0.0]
+    assert h.poly_seg[h.poly_offsets[0]:h.poly_offsets[1]].tolist() == [0.0, 0.55901699437494734, 1.1102230246251565e-16]
+    assert h.term[3] == 1 and h.traced[3] == 0.50062460986251966
+    assert h.errors == [(4, "initial direction is normal to the anchor face"), (6, "trace: start face out of range"),
+                        (8, "trace: start barycentric coordinates not in the simplex"),
+                        (9, "trace: start face out of range")]
+
+
+def test_concat_meshes_stay_on_component(gpu, ref):
+    ra, rb = ref.RefMesh.icosphere(2), ref.RefMesh.torus(1 / 3, 1 / 6, 24, 12)
+    rm = ref.RefMesh.concat(ra, rb)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(2, 5000, 0.1, 2.0)
+    r, h = both(rm, m, f, b, d)
+    assert_trace_equal(r, h, len(f))
+    assert ((f < ra.nf) == (h.face < ra.nf)).all()
+
+
+def test_empty_and_single(gpu, ref):
+    rm = ref.RefMesh.icosphere(1)
+    m = gpu_mesh(gpu, rm)
+    e = m.trace_batch(np.empty(0, np.int32), np.empty((0, 3)), np.empty((0, 3)), record_polyline=True)
+    assert len(e.face) == 0 and e.total_crossings == 0
+    f, b, d = rm.sample_queries(3, 1, 1.0, 1.0)
+    r, h = both(rm, m, f, b, d)
+    assert_trace_equal(r, h, 1)
+
+
+def test_invalid_batch_arguments(gpu, ref):
+    m = gpu_mesh(gpu, ref.RefMesh.icosphere(1))
+    with pytest.raises(gpu.DgError) as e:
+        m.trace_batch(np.zeros(3, np.int32), np.zeros((2, 3)), np.zeros((3, 3)))
+    assert e.value.klass == "InvalidArgs"
+    with pytest.raises(gpu.DgError):
+        m.trace_batch(np.zeros(3, np.int32), np.zeros((3, 3)), np.zeros((3, 3)), payload=np.zeros((2, 3)))
+
+
+def test_run_to_run_and_shape_determinism(gpu, ref):
+    """Results are bitwise independent of the launch shape (the reference's worker-count contract)."""
+    rm = ref.RefMesh.icosphere(5)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(8, 30000, 0.05, 4.0)
+    base = m.trace_batch(f, b, d)
+    for kw in (dict(), dict(blocks_per_sm=1), dict(refill_min=16), dict(sort_by_face=True)):
+        o = m.trace_batch(f, b, d, **kw)
+        for k in ("face", "bary", "dir", "traced", "term", "status", "crossings"):
+            assert np.array_equal(getattr(base, k), getattr(o, k)), (k, kw)
+
+
+def test_full_size_invariants_1m_face_torus(gpu):
+    """BASELINE-size mesh (1 M faces): size-independent properties of the exponential map --
+    requested length is consumed exactly, barycentrics stay on the simplex, directions are unit
+    and tangent, and reversing the final direction returns to the start (geodesic reversibility)."""
+    from paper_2603_15780_b200 import workloads as W
+    xyz, tri = W.torus(1 / 3, 1 / 6, 1000, 500)
+    m = gpu.Mesh(xyz, tri)
+    n = 200000
+    diag = W.bbox_diagonal(xyz)
+    f, b, d = W.sample_queries(xyz, tri, n, 0.25 * diag, seed=4)
+    h = m.trace_batch(f, b, d)
+    assert (h.status == 0).all() and (h.term == 0).all()
+    assert np.abs(h.traced - h.requested).max() <= 1e-12 * diag
+    assert np.abs(h.bary.sum(1) - 1).max() <= 1e-12 and h.bary.min() >= 0
+    assert np.abs(np.linalg.norm(h.dir, axis=1) - 1).max() <= 1e-12
+    assert np.abs(np.einsum("nd,nd->n", h.dir, m.fnormal[h.face])).max() <= 1e-9
+    back = m.trace_batch(h.face, h.bary, -h.dir * h.requested[:, None])
+    ok = back.status == 0
+    err = np.linalg.norm(m.embed(back.face[ok], back.bary[ok]) - m.embed(f[ok], b[ok]), axis=1)
+    # vertex-free straightest geodesics are reversible up to rounding
+    assert np.quantile(err, 0.999) <= 1e-9 * diag
+    assert h.total_crossings > 300 * n
