@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libdigeo_b200.so")
+LIB_PATH = os.environ.get("DG_B200_LIB") or os.path.join(PKG, "lib", "libdigeo_b200.so")
 
 DG_OK = 0
 ERR_NAMES = {1: "InvalidArgs", 2: "CudaError", 3: "ParseError", 4: "NonManifoldError",

@@ -14,7 +14,19 @@ namespace dg {
 
 namespace {
 
-constexpr int kBlockThreads = 128;
+#ifndef DG_TRACE_BLOCK
+#define DG_TRACE_BLOCK 128
+#endif
+// Resident CTAs per SM the register allocation is capped for. The lite f64 walker fits 128
+// registers (4 CTAs x 4 warps per SM) with ~50 bytes of spill and is 17% faster there than at its
+// natural 146 registers / 3 CTAs (profiles/tuning_r1.md); the full variant (212 registers) keeps 2 CTAs.
+#ifndef DG_TRACE_MIN_BLOCKS
+#define DG_TRACE_MIN_BLOCKS 4
+#endif
+#ifndef DG_TRACE_MIN_BLOCKS_FULL
+#define DG_TRACE_MIN_BLOCKS_FULL 2
+#endif
+constexpr int kBlockThreads = DG_TRACE_BLOCK;
 constexpr unsigned kFullMask = 0xffffffffu;
 
 template <class S, bool kFull>
@@ -54,7 +66,7 @@ __device__ __forceinline__ void write_result(const TraceParams& p, int64_t q,
 }
 
 template <class S, bool kFull>
-__global__ void __launch_bounds__(kBlockThreads) trace_kernel(const __grid_constant__ TraceParams p) {
+__global__ void __launch_bounds__(kBlockThreads, kFull ? DG_TRACE_MIN_BLOCKS_FULL : DG_TRACE_MIN_BLOCKS) trace_kernel(const __grid_constant__ TraceParams p) {
   Tracer<S, kFull> T(p.mesh, p.max_steps, p.hole_avoidance != 0);
   const unsigned lane = threadIdx.x & 31u;
   const unsigned long long n = (unsigned long long)p.n;

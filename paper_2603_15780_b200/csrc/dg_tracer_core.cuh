@@ -195,7 +195,7 @@ struct Tracer {
     if (bary.y <= Tol<S>::bary()) bary.y = S(0);
     if (bary.z <= Tol<S>::bary()) bary.z = S(0);
     S s = bary.x + bary.y + bary.z;
-    if (s > S(0)) bary = bary / s;
+    if (s > S(0)) bary = div_pos(bary, s);
     const S hi = S(1) - Tol<S>::bary();
     if (bary.x >= hi) bary = unit_axis<S>(0);
     else if (bary.y >= hi) bary = unit_axis<S>(1);
@@ -214,6 +214,18 @@ struct Tracer {
     return Outcome::Stalled;
   }
 
+  // lambda = max(0, -b / v) of tracer.cpp:190-191 for a candidate (v < 0, b >= +0), computed so
+  // that no lane ever divides a zero (CUDA's f64 division takes a long slow path for a zero
+  // quotient, and b is exactly 0 for the corner opposite the entry edge): (-0)/v is +0 for v < 0.
+  // Lanes without a candidate in this slot (valid == false) divide 1 by -1 and are ignored.
+  static DG_HD S exit_param(S b, S v, bool valid) {
+    const bool z = !valid || b == S(0);
+    const S q = nonzero_numerator(valid ? -b : S(0), z) / (valid ? v : S(-1));
+    S lambda = z ? S(0) : q;
+    if (lambda < S(0)) lambda = S(0);
+    return lambda;
+  }
+
   // tracer.cpp:177-223
   DG_HD Outcome advance() {
     S bv1, bv2;
@@ -224,21 +236,25 @@ struct Tracer {
     if (!dg_finite(double(scale)) || scale <= S(0)) return stall(kStallDegenerateDir);
     S tol = Tol<S>::dir_rel() * scale;
 
+    // Exit candidates are the components with bv_i < -tol, scanned in index order with a strict
+    // '<' (first wins ties), tracer.cpp:186-196. The velocity sums to zero, so at most two
+    // components qualify: the two candidate quotients are computed in two branch-free slots
+    // (A = lowest candidate index, B = the next one) instead of three divergent branches.
+    const bool c0 = !(bv.x >= -tol), c1 = !(bv.y >= -tol), c2 = !(bv.z >= -tol);
+    const int ia = c0 ? 0 : (c1 ? 1 : (c2 ? 2 : -1));
+    const int ib = c0 ? (c1 ? 1 : (c2 ? 2 : -1)) : ((c1 && c2) ? 2 : -1);
     S best = dg_inf<S>();
     int exit_edge = -1;
-    if (!(bv.x >= -tol)) {
-      S lambda = -bary.x / bv.x;
-      if (lambda < S(0)) lambda = S(0);
-      if (lambda < best) { best = lambda; exit_edge = 0; }
+    {
+      const S lambda = exit_param(get(bary, ia), get(bv, ia), ia >= 0);
+      if (ia >= 0 && lambda < best) { best = lambda; exit_edge = ia; }
     }
-    if (!(bv.y >= -tol)) {
-      S lambda = -bary.y / bv.y;
-      if (lambda < S(0)) lambda = S(0);
-      if (lambda < best) { best = lambda; exit_edge = 1; }
+    {
+      const S lambda = exit_param(get(bary, ib), get(bv, ib), ib >= 0);
+      if (ib >= 0 && lambda < best) { best = lambda; exit_edge = ib; }
     }
-    if (!(bv.z >= -tol)) {
-      S lambda = -bary.z / bv.z;
-      if (lambda < S(0)) lambda = S(0);
+    if (c0 && c1 && c2) {  // unreachable for finite inputs; kept for exact reference semantics
+      const S lambda = exit_param(bary.z, bv.z, true);
       if (lambda < best) { best = lambda; exit_edge = 2; }
     }
     if (exit_edge < 0) return stall(kStallNoExit);
