@@ -240,6 +240,15 @@ int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf
 #define DG_TRY(expr) if ((e = (expr)) != cudaSuccess) return cleanup(fail_cuda(e, #expr))
   DG_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, g_device));
   DG_TRY(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  {
+    // Staging buffers come from the device's stream-ordered pool; keep freed blocks cached so
+    // that a DG_MEM_HOST call does not pay for physical allocation on every invocation.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, g_device) == cudaSuccess) {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   const size_t F = size_t(nf), Vn = size_t(nv);
   DG_TRY(cudaMalloc(&m->rec, F * sizeof(dg::FaceRec)));
   DG_TRY(cudaMalloc(&m->fnormal, 3 * F * sizeof(double)));

@@ -176,8 +176,7 @@ struct Tracer {
     S g11 = dot(e1, e1), g12 = dot(e1, e2), g22 = dot(e2, e2);
     S det = g11 * g22 - g12 * g12;
     S r1 = dot(e1, w), r2 = dot(e2, w);
-    *c1 = (g22 * r1 - g12 * r2) / det;
-    *c2 = (g11 * r2 - g12 * r1) / det;
+    div_pair(g22 * r1 - g12 * r2, g11 * r2 - g12 * r1, det, c1, c2);
   }
   // tracer.cpp:140-146
   static DG_HD bool wedge_contains(const Face<S>& g, int k, const V3<S>& w) {

@@ -1,0 +1,133 @@
+"""CPU tier: pins the plain-C oracle (oracle/digeo_oracle.c) and the host-compiled device state
+machine (tests/hostcheck) against (1) the golden fixtures generated from the unmodified
+reference (tests/golden/*.npz, made by tests/golden/make_golden.py), (2) the reference's own
+golden trace values (proj/tests/golden/trace_square.json, restated below) and (3) -- when
+oracle/_ref is present -- the reference itself on fresh seeded inputs."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+TRACE_FIXTURES = sorted(p for p in glob.glob(os.path.join(HERE, "golden", "*.npz")) if "diff" not in p)
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    import __graft_entry__  # noqa: F401
+    import oracle_api
+    if not oracle_api.available():
+        import subprocess
+        subprocess.check_call(["make", "-C", os.path.join(os.path.dirname(HERE), "oracle"), "liboracle.so"])
+    return oracle_api
+
+
+@pytest.fixture(scope="session")
+def hostcheck():
+    import hostcheck_api
+    hostcheck_api.build()
+    return hostcheck_api
+
+
+def _equal(a, b):
+    return bool(((a == b) | (np.isnan(a) & np.isnan(b))).all())
+
+
+def check_against_fixture(z, r, exact):
+    n = len(z["face"])
+    for k in ("face", "term", "status", "npoints"):
+        assert np.array_equal(z["o_" + k], getattr(r, k)), k
+    assert np.array_equal(z["poly_face"], r.poly_face), "face sequence"
+    pairs = [("o_bary", r.bary), ("o_dir", r.dir), ("o_traced", r.traced), ("o_requested", r.requested),
+             ("poly_bary", r.poly_bary), ("poly_seg", r.poly_seg)]
+    if z["payload"].size:
+        pairs.append(("o_payload", r.payload))
+    if z["cfg"][2]:
+        pairs.append(("o_q", r.q))
+    for k, got in pairs:
+        if exact:
+            assert _equal(z[k], got), f"{k} not bit-equal ({n} traces)"
+        else:
+            assert np.nanmax(np.abs(z[k] - got)) <= 1e-12, k
+
+
+@pytest.mark.parametrize("path", TRACE_FIXTURES, ids=[os.path.basename(p)[:-4] for p in TRACE_FIXTURES])
+def test_oracle_matches_reference_fixtures(oracle, path):
+    z = np.load(path)
+    m = oracle.OracleMesh(z["xyz"], z["tri"])
+    assert np.array_equal(m.arrays()["adj"], z["adj"]) and np.array_equal(m.arrays()["vangle"], z["vangle"])
+    assert m.mean_edge == float(z["mean_edge"])
+    pay = z["payload"] if z["payload"].size else None
+    r = m.trace_batch(z["face"], z["bary"], z["dir"], payload=pay, max_steps=int(z["cfg"][0]),
+                      hole_avoidance=bool(z["cfg"][1]), want_q=bool(z["cfg"][2]), record_polyline=True)
+    check_against_fixture(z, r, exact=True)  # same libm on the host: bit-exact including vertex branches
+
+
+@pytest.mark.parametrize("path", TRACE_FIXTURES, ids=[os.path.basename(p)[:-4] for p in TRACE_FIXTURES])
+def test_device_state_machine_on_host_matches_fixtures(hostcheck, oracle, path):
+    """The kernel's state machine (dg_tracer_core.cuh) compiled for the host reproduces the
+    reference fixtures bit for bit -- control flow and arithmetic are checked before any GPU time."""
+    z = np.load(path)
+    a = oracle.OracleMesh(z["xyz"], z["tri"]).arrays()
+    hm = hostcheck.HostMesh(a)
+    pay = z["payload"] if z["payload"].size else None
+    r = hm.trace_batch(z["face"], z["bary"], z["dir"], payload=pay, max_steps=int(z["cfg"][0]),
+                       hole_avoidance=bool(z["cfg"][1]), want_q=bool(z["cfg"][2]), record_polyline=True)
+    check_against_fixture(z, r, exact=True)
+
+
+def test_golden_square_trace_values(oracle):
+    """proj/tests/golden/trace_square.json, compared bit-for-bit by the reference (test_io.cpp:71-82)."""
+    m = oracle.OracleMesh([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]], [[0, 1, 2], [0, 2, 3]])
+    r = m.trace_batch([0], [[.5, .25, .25]], [[.25, .5, 0]], record_polyline=True)
+    assert r.face[0] == 1 and r.bary[0].tolist() == [0.24999999999999992, 0.75000000000000011, 0.0]
+    assert r.poly_face.tolist() == [0, 0, 1]
+    assert r.poly_bary.tolist() == [[.5, .25, .25], [.25, 0.0, .75], [0.24999999999999992, 0.75000000000000011, 0.0]]
+    assert r.poly_seg.tolist() == [0.0, 0.55901699437494734, 1.1102230246251565e-16]
+    assert r.dir[0].tolist() == [0.44721359549995771, 0.89442719099991608, 0.0]
+    assert r.term[0] == 0 and r.status[0] == 0
+    # boundary stop known answer
+    r = m.trace_batch([0], [[.5, .25, .25]], [[2, .1, 0]])
+    assert r.term[0] == 1 and r.bary[0].tolist() == [0.0, 0.72500000000000009, 0.27499999999999997]
+    assert r.traced[0] == 0.50062460986251966 and r.requested[0] == 2.0024984394500787
+
+
+def test_oracle_differentials_match_fixture(oracle):
+    z = np.load(os.path.join(HERE, "golden", "ico3_diff.npz"))
+    m = oracle.OracleMesh(z["xyz"], z["tri"])
+    ep = m.ep(z["face"], z["bary"], z["dir"], z["end_face"], z["end_bary"], z["end_dir"], g=z["g"])
+    assert np.array_equal(ep["rot"], z["ep_rot"]) and np.array_equal(ep["frames"], z["ep_frames"])
+    assert np.array_equal(ep["grad_v"], z["ep_grad_v"]) and not ep["grad_p"].any()
+    assert m.default_gfd_eps() == float(z["eps"])
+    gfd = m.gfd(z["face"], z["bary"], z["dir"], g=z["g"])
+    for k in ("jv", "jp", "degraded", "frames", "grad_v", "grad_p"):
+        assert np.array_equal(gfd[k], z["gfd_" + k]), k
+
+
+def test_oracle_error_classes(oracle):
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.OracleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [0, -1, 0]], [[0, 1, 2], [0, 1, 3], [1, 0, 4]])
+    assert e.value.klass == "NonManifoldError" and e.value.msg == "edge (0,1) incident to 3+ faces"
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.OracleMesh([[0, 0, 0], [1, 0, 0], [2, 0, 0]], [[0, 1, 2]])
+    assert e.value.klass == "DegenerateFaceError" and e.value.msg == "face 0 has zero area"
+
+
+def test_oracle_vs_reference_fresh_inputs(oracle, ref):
+    """Differential check against the unmodified reference on inputs that are not in the fixtures."""
+    for rm, seed, lo, hi in ((ref.RefMesh.icosphere(3), 77, 0.1, 3.0), (ref.RefMesh.torus(1 / 3, 1 / 6, 40, 20), 78, 0.05, 2.0),
+                             (ref.RefMesh.cylinder(0.5, 1.0, 16, 4), 79, 0.05, 3.0)):
+        a = rm.arrays()
+        m = oracle.OracleMesh(a["xyz"], a["tri"])
+        for k in ("adj", "fnormal", "farea", "vangle", "varea", "vboundary", "csr_off", "csr_list"):
+            assert np.array_equal(m.arrays()[k], a[k]), k
+        f, b, d = rm.sample_queries(seed, 3000, lo, hi)
+        pay = np.random.default_rng(seed).normal(size=(len(f), 3))
+        for hole in (False, True):
+            r = rm.trace_batch(f, b, d, payload=pay, want_q=True, record_polyline=True, hole_avoidance=hole)
+            o = m.trace_batch(f, b, d, payload=pay, want_q=True, record_polyline=True, hole_avoidance=hole)
+            for k in ("face", "bary", "dir", "traced", "term", "status", "npoints", "payload", "q", "poly_face",
+                      "poly_bary", "poly_seg"):
+                assert _equal(np.asarray(getattr(r, k), float), np.asarray(getattr(o, k), float)), (k, hole)
+            assert r.errors == o.errors
