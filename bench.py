@@ -170,6 +170,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:   # functional test of the N>1 path on a 1-GPU box (ranks share device 0)
+        local = 0
     if dg.device_count() == 0:
         raise SystemExit("bench.py: no CUDA device (there is no CPU fallback)")
     torch.cuda.set_device(local)
@@ -177,7 +179,10 @@ def run_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     wl = WORKLOADS[args.workload]
     scheme = wl["scheme"]
@@ -355,6 +360,8 @@ def main():
     ap.add_argument("--geodesics", type=int, default=0, help="geodesics per GPU (default: the workload's)")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (nccl on the GPU box)")
+    ap.add_argument("--share-gpu", action="store_true", help="testing only: all ranks use cuda:0 (with --dist-backend gloo)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

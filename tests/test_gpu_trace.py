@@ -209,3 +209,55 @@ def test_full_size_invariants_1m_face_torus(gpu):
     # vertex-free straightest geodesics are reversible up to rounding
     assert np.quantile(err, 0.999) <= 1e-9 * diag
     assert h.total_crossings > 300 * n
+
+
+def test_config4_style_heterogeneous_batch_mixed_lengths(gpu, ref):
+    """BASELINE config 4 (scaled down): several meshes concatenated into one (mesh.cpp:199-206),
+    queries on every component, lengths log-uniform over two decades (divergence stress)."""
+    parts = [ref.RefMesh.icosphere(3), ref.RefMesh.torus(1 / 3, 1 / 6, 40, 20), ref.RefMesh.icosphere(2),
+             ref.RefMesh.torus(0.5, 0.2, 24, 12)]
+    rm = parts[0]
+    for p in parts[1:]:
+        rm = ref.RefMesh.concat(rm, p)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(21, 20000, 1.0, 1.0)
+    rng = np.random.default_rng(4)
+    d *= np.exp(rng.uniform(np.log(0.01), np.log(4.0), len(f)))[:, None]
+    r, h = both(rm, m, f, b, d)
+    assert_trace_equal(r, h, len(f))
+    assert h.crossings.max() > 50 * max(1, np.median(h.crossings)) / 10
+
+
+def test_config5_style_long_vertex_heavy_traces(gpu, ref):
+    """BASELINE config 5 (scaled down): starts exactly at vertices aimed exactly along an edge,
+    length 5 x the outer diameter, explicit max_steps on both sides; half random starts."""
+    rm = ref.RefMesh.torus(1 / 3, 1 / 6, 100, 50)
+    m = gpu_mesh(gpu, rm)
+    a = rm.arrays()
+    X, T = a["xyz"], a["tri"]
+    n = 600
+    rng = np.random.default_rng(6)
+    fs = rng.integers(0, rm.nf, n).astype(np.int32)
+    bs = np.zeros((n, 3))
+    bs[:, 0] = 1
+    ds = X[T[fs, 1]] - X[T[fs, 0]]
+    ds *= (5.0 / np.linalg.norm(ds, axis=1))[:, None]
+    f2, b2, d2 = rm.sample_queries(3, n, 5.0, 5.0)
+    F, B, D = np.concatenate([fs, f2]), np.concatenate([bs, b2]), np.concatenate([ds, d2])
+    r = rm.trace_batch(F, B, D, record_polyline=True, max_steps=200000)
+    h = m.trace_batch(F, B, D, record_polyline=True, max_steps=200000)
+    diag = np.linalg.norm(X.max(0) - X.min(0))
+    assert_trace_equal(r, h, len(F), exact=False, tol=1e-9 * diag)
+    vertex_points = (h.poly_bary == 1).any(1).sum()
+    assert vertex_points > 3 * n           # the walks really pass through vertices
+    assert (h.term == 0).all() and np.abs(h.traced - 5.0).max() < 1e-9
+
+
+def test_default_max_steps_termination_matches(gpu, ref):
+    """MaxSteps must trigger on the same step as the reference (a vertex crossing costs 2 steps)."""
+    rm = ref.RefMesh.icosphere(2)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(13, 3000, 30.0, 60.0)   # far longer than 10*sqrt(F)+100 crossings
+    r, h = both(rm, m, f, b, d)
+    assert (h.term == 2).any()
+    assert_trace_equal(r, h, len(f))
