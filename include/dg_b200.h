@@ -103,6 +103,16 @@ DG_API int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int
                           const int32_t* adj, const double* fnormal, const double* vangle,
                           const uint8_t* vboundary, const int32_t* csr_off,
                           const int32_t* csr_list, dg_mesh** out);
+/* Same, with layout flags. The transport cache stores, per directed half-edge, the fold isometry
+ * of tracer.cpp:113-126 (96 B per half-edge, computed on the device at upload by the same code the
+ * uncached walker runs, so results are bit-identical): AUTO enables it when face records + cache
+ * fit in 3/4 of the L2 (env DG_TRANSPORT_CACHE=on|off|auto overrides AUTO). */
+enum { DG_MESH_TRANSPORT_AUTO = 0, DG_MESH_TRANSPORT_ON = 1, DG_MESH_TRANSPORT_OFF = 2 };
+DG_API int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf,
+                             const int32_t* adj, const double* fnormal, const double* vangle,
+                             const uint8_t* vboundary, const int32_t* csr_off,
+                             const int32_t* csr_list, uint32_t flags, dg_mesh** out);
+DG_API int dg_mesh_has_transport_cache(const dg_mesh* m);
 DG_API void dg_mesh_destroy(dg_mesh* m);
 DG_API int32_t dg_mesh_face_count(const dg_mesh* m);
 DG_API int32_t dg_mesh_vertex_count(const dg_mesh* m);
@@ -160,8 +170,9 @@ typedef struct dg_trace_out {
 DG_API int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in,
                           const dg_trace_cfg* cfg, dg_trace_out* out);
 
-/* Registers per thread, resident CTAs per SM and CTA size of a tracer kernel variant
- * (full = payload / transport matrix / hole avoidance / polyline support compiled in). */
+/* Registers per thread, resident CTAs per SM and CTA size of a tracer kernel variant.
+ * full: bit 0 = payload / transport matrix / hole avoidance / polyline support compiled in,
+ *       bit 1 = transport-cache variant. */
 DG_API void dg_trace_kernel_info(int use_f32, int full, int* regs, int* blocks_per_sm,
                                  int* block_threads);
 

@@ -59,8 +59,10 @@ class Mesh:
     """Immutable triangle mesh: host-side derived arrays (Mesh::build, mesh.cpp:34-130) plus
     the GPU-resident fat-record store (dg_mesh_create)."""
 
-    def __init__(self, xyz, tri, device=None, upload=True):
+    def __init__(self, xyz, tri, device=None, upload=True, transport_cache="auto"):
         L = lib()
+        self.transport_cache = transport_cache
+        self.has_transport_cache = False
         self.xyz = _f64(xyz).reshape(-1, 3)
         self.tri = _i32(tri).reshape(-1, 3)
         nv, nf = len(self.xyz), len(self.tri)
@@ -92,10 +94,12 @@ class Mesh:
         if device is not None:
             check(L.dg_set_device(int(device)))
         h = C.c_void_p(0)
-        check(L.dg_mesh_create(ptr(self.xyz), self.nv, ptr(self.tri), self.nf, ptr(self.adj), ptr(self.fnormal),
-                               ptr(self.vangle), ptr(self.vboundary), ptr(self.csr_off), ptr(self.csr_list),
-                               C.addressof(h)))
+        flags = {"auto": 0, None: 0, True: 1, "on": 1, False: 2, "off": 2}[self.transport_cache]
+        check(L.dg_mesh_create_ex(ptr(self.xyz), self.nv, ptr(self.tri), self.nf, ptr(self.adj), ptr(self.fnormal),
+                                  ptr(self.vangle), ptr(self.vboundary), ptr(self.csr_off), ptr(self.csr_list),
+                                  flags, C.addressof(h)))
         self.h = h
+        self.has_transport_cache = bool(L.dg_mesh_has_transport_cache(h))
         return self
 
     def __del__(self):
@@ -283,7 +287,8 @@ class Mesh:
                                      ptr(grad_v), ptr(grad_p), None, None, None, C.addressof(ei)), ei)
 
 
-def kernel_info(use_f32=False, full=False):
+def kernel_info(use_f32=False, full=False, cached=False):
     regs, bps, bt = C.c_int(0), C.c_int(0), C.c_int(0)
-    lib().dg_trace_kernel_info(int(use_f32), int(full), C.addressof(regs), C.addressof(bps), C.addressof(bt))
+    lib().dg_trace_kernel_info(int(use_f32), int(full) | (int(cached) << 1), C.addressof(regs), C.addressof(bps),
+                               C.addressof(bt))
     return dict(registers=regs.value, blocks_per_sm=bps.value, block_threads=bt.value)

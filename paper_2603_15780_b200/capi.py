@@ -35,7 +35,7 @@ STALL_MESSAGES = {
 
 EXPORTS = [
     "dg_last_error", "dg_version", "dg_device_count", "dg_set_device", "dg_device_sm_count",
-    "dg_mesh_derive", "dg_mesh_create", "dg_mesh_destroy", "dg_mesh_face_count", "dg_mesh_vertex_count",
+    "dg_mesh_derive", "dg_mesh_create", "dg_mesh_create_ex", "dg_mesh_has_transport_cache", "dg_mesh_destroy", "dg_mesh_face_count", "dg_mesh_vertex_count",
     "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_transition", "dg_ep_jacobians",
     "dg_ep_backward", "dg_gfd_jacobians", "dg_trace_kernel_info",
 ]
@@ -95,6 +95,8 @@ def lib():
         vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
         L.dg_mesh_derive.argtypes = [vp, i32, vp, i32] + [vp] * 11
         L.dg_mesh_create.argtypes = [vp, i32, vp, i32] + [vp] * 7
+        L.dg_mesh_create_ex.argtypes = [vp, i32, vp, i32] + [vp] * 6 + [C.c_uint32, vp]
+        L.dg_mesh_has_transport_cache.argtypes = [vp]
         L.dg_trace_batch.argtypes = [vp, i64, vp, vp, vp]
         L.dg_transition.argtypes = [vp, C.c_int, i64, vp, vp, vp, vp, C.c_int] + [vp] * 8
         L.dg_ep_jacobians.argtypes = [vp, i64] + [vp] * 10

@@ -3,9 +3,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "dg_capi_common.hpp"
+#include "dg_tracer_core.cuh"
 
 namespace dgapi {
 
@@ -51,6 +53,32 @@ __global__ void build_records_kernel(const double* __restrict__ xyz, const int32
     r.x[3 * k + 2] = xyz[3 * size_t(v) + 2];
   }
   rec[f] = r;
+}
+
+// Transport cache: one thread per directed half-edge runs the reference's make_edge_transport
+// (tracer.cpp:113-126) through the very functions the uncached walker uses, so cached and
+// uncached traces are bit-identical.
+__global__ void build_halfedges_kernel(const dg::MeshView m, dg::HalfEdgeRec* he) {
+  using namespace dg;
+  const int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (s >= 3 * int64_t(m.nf)) return;
+  const int f = int(s / 3), k = int(s % 3);
+  const Face<double> c = load_face<double>(m, f);
+  HalfEdgeRec r{};
+  r.g = c.adj(k);
+  if (r.g >= 0) {
+    const int ka = (k + 1) % 3, kc = (k + 2) % 3;
+    const int va = c.id(ka), vc = c.id(kc);
+    const Face<double> G = load_face<double>(m, r.g);
+    const int vt = G.third(va, vc);
+    const EdgeTransport<double> t =
+        Tracer<double, false>::make_edge_transport(c.pos(ka), c.pos(kc), c.pos(k), G.pos_of(vt));
+    r.t[0] = t.edge.x; r.t[1] = t.edge.y; r.t[2] = t.edge.z;
+    r.t[3] = t.in_from.x; r.t[4] = t.in_from.y; r.t[5] = t.in_from.z;
+    r.t[6] = t.in_to.x; r.t[7] = t.in_to.y; r.t[8] = t.in_to.z;
+    r.corners = G.corner_of(va) | (G.corner_of(vc) << 2) | (G.corner_of(vt) << 4);
+  }
+  he[s] = r;
 }
 
 __global__ void iota_kernel(int32_t* a, int64_t n) {
@@ -223,6 +251,13 @@ int dg_mesh_derive(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf
 int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf, const int32_t* adj,
                    const double* fnormal, const double* vangle, const uint8_t* vboundary,
                    const int32_t* csr_off, const int32_t* csr_list, dg_mesh** out) {
+  return dg_mesh_create_ex(xyz, nv, tri, nf, adj, fnormal, vangle, vboundary, csr_off, csr_list,
+                           DG_MESH_TRANSPORT_AUTO, out);
+}
+
+int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf, const int32_t* adj,
+                      const double* fnormal, const double* vangle, const uint8_t* vboundary,
+                      const int32_t* csr_off, const int32_t* csr_list, uint32_t flags, dg_mesh** out) {
   if (!out) return fail(DG_ERR_INVALID_ARGS, "dg_mesh_create: null output handle");
   *out = nullptr;
   if (nv <= 0 || nf <= 0 || !xyz || !tri || !adj || !fnormal || !vangle || !vboundary || !csr_off || !csr_list)
@@ -258,6 +293,24 @@ int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf
   DG_TRY(cudaMalloc(&m->vboundary, Vn));
   DG_TRY(cudaMalloc(&m->counters, 2 * dg_mesh::kRing * sizeof(unsigned long long)));
   m->bytes = int64_t(F * sizeof(dg::FaceRec) + 3 * F * 8 + Vn * 8 + (Vn + 1) * 4 + 3 * F * 4 + Vn);
+  // Transport cache policy: AUTO keeps records + cache (384 B per face) inside ~3/4 of the L2.
+  bool cache = (flags & 3u) == DG_MESH_TRANSPORT_ON;
+  if ((flags & 3u) == DG_MESH_TRANSPORT_AUTO) {
+    const char* env = getenv("DG_TRANSPORT_CACHE");
+    if (env && (!strcmp(env, "on") || !strcmp(env, "1"))) {
+      cache = true;
+    } else if (env && (!strcmp(env, "off") || !strcmp(env, "0"))) {
+      cache = false;
+    } else {
+      int l2 = 0;
+      cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g_device);
+      cache = F * (sizeof(dg::FaceRec) + 3 * sizeof(dg::HalfEdgeRec)) <= size_t(l2) / 4 * 3;
+    }
+  }
+  if (cache) {
+    DG_TRY(cudaMalloc(&m->he, 3 * F * sizeof(dg::HalfEdgeRec)));
+    m->bytes += int64_t(3 * F * sizeof(dg::HalfEdgeRec));
+  }
 
   // indexed arrays are only needed to assemble the records
   double* d_xyz = nullptr;
@@ -269,6 +322,10 @@ int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf
   DG_TRY(cudaMemcpyAsync(d_tri, tri, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(d_adj, adj, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(dg::launch_build_records(d_xyz, d_tri, d_adj, nf, m->rec, m->stream));
+  if (m->he) {
+    build_halfedges_kernel<<<unsigned((3 * F + 127) / 128), 128, 0, m->stream>>>(m->view_uncached(), m->he);
+    DG_TRY(cudaGetLastError());
+  }
   DG_TRY(cudaMemcpyAsync(m->fnormal, fnormal, 3 * F * sizeof(double), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(m->vangle, vangle, Vn * sizeof(double), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(m->csr_off, csr_off, (Vn + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
@@ -288,12 +345,13 @@ void dg_mesh_destroy(dg_mesh* m) {
   if (!m) return;
   DeviceGuard guard(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
-  cudaFree(m->rec); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
+  cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
   cudaFree(m->csr_list); cudaFree(m->vboundary); cudaFree(m->counters);
   if (m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }
 
+int dg_mesh_has_transport_cache(const dg_mesh* m) { return m && m->he ? 1 : 0; }
 int32_t dg_mesh_face_count(const dg_mesh* m) { return m ? m->nf : 0; }
 int32_t dg_mesh_vertex_count(const dg_mesh* m) { return m ? m->nv : 0; }
 int64_t dg_mesh_device_bytes(const dg_mesh* m) { return m ? m->bytes : 0; }
@@ -404,7 +462,7 @@ void dg_trace_kernel_info(int use_f32, int full, int* regs, int* blocks_per_sm, 
   if (block_threads) *block_threads = 0;
   if (dg_device_count() == 0) return;
   DeviceGuard guard(g_device);
-  dg::trace_kernel_info(use_f32 != 0, full != 0, regs, blocks_per_sm, block_threads);
+  dg::trace_kernel_info(use_f32 != 0, full, regs, blocks_per_sm, block_threads);
 }
 
 }  // extern "C"

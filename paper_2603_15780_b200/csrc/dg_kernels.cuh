@@ -53,7 +53,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
                          cudaStream_t stream);
 
 // Kernel attributes for reporting (registers, max resident blocks per SM).
-void trace_kernel_info(bool use_f32, bool full, int* regs, int* blocks_per_sm, int* block_threads);
+void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads);
 
 // ---- differentials (dg_diff_kernels.cu) ---------------------------------------------------
 

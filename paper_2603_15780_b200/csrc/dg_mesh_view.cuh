@@ -24,8 +24,22 @@ struct alignas(32) FaceRec {
 };
 static_assert(sizeof(FaceRec) == 96, "FaceRec must be three 32-byte sectors");
 
+// Optional per-directed-half-edge transport cache (slot 3 f + k = crossing face f through the
+// edge opposite corner k). The fold isometry of tracer.cpp:113-126 depends only on the mesh, so
+// it is computed once at upload -- by the same device functions the uncached walker runs, hence
+// bit-identical -- and a crossing becomes two gathers with no sqrt / normalisation of edge
+// frames. 80 useful bytes, padded to three 32-byte sectors.
+struct alignas(32) HalfEdgeRec {
+  double t[9];      // edge, in_from, in_to (unit vectors)
+  int32_t g;        // face entered (-1 = boundary)
+  int32_t corners;  // ja | jc << 2 | jt << 4: corners of va, vc and of the third vertex in g
+  int32_t pad[4];
+};
+static_assert(sizeof(HalfEdgeRec) == 96, "HalfEdgeRec must be three 32-byte sectors");
+
 struct MeshView {
   const FaceRec* rec;        // [nf]
+  const HalfEdgeRec* he;     // [3 nf] or null (transport cache off)
   const double* fnormal;     // [3 nf] unit face normals                  (Mesh::face_normals)
   const double* vangle;      // [nv]   total interior angle per vertex    (Mesh::vertex_total_angle)
   const int32_t* csr_off;    // [nv+1] vertex -> incident faces, face order (mesh.cpp:118-127)
@@ -89,6 +103,33 @@ DG_HD Face<S> load_face(const MeshView& m, int f) {
   r.a0 = c.adj[0]; r.a1 = c.adj[1]; r.a2 = c.adj[2];
 #endif
   return r;
+}
+
+struct HalfEdge {
+  V3<double> edge, in_from, in_to;
+  int g, ja, jc, jt;
+};
+DG_HD HalfEdge load_halfedge(const MeshView& m, int f, int k) {
+  HalfEdge h;
+  const HalfEdgeRec* r = m.he + (3 * size_t(f) + size_t(k));
+#ifdef __CUDA_ARCH__
+  const double2* p = reinterpret_cast<const double2*>(r);
+  double2 d0 = __ldg(p + 0), d1 = __ldg(p + 1), d2 = __ldg(p + 2), d3 = __ldg(p + 3);
+  int4 w = __ldg(reinterpret_cast<const int4*>(p + 4));
+  h.edge = {d0.x, d0.y, d1.x};
+  h.in_from = {d1.y, d2.x, d2.y};
+  h.in_to = {d3.x, d3.y, __hiloint2double(w.y, w.x)};
+  h.g = w.z;
+  const int c = w.w;
+#else
+  h.edge = {r->t[0], r->t[1], r->t[2]};
+  h.in_from = {r->t[3], r->t[4], r->t[5]};
+  h.in_to = {r->t[6], r->t[7], r->t[8]};
+  h.g = r->g;
+  const int c = r->corners;
+#endif
+  h.ja = c & 3; h.jc = (c >> 2) & 3; h.jt = (c >> 4) & 3;
+  return h;
 }
 
 template <class S>

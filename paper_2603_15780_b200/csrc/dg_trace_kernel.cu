@@ -29,9 +29,9 @@ namespace {
 constexpr int kBlockThreads = DG_TRACE_BLOCK;
 constexpr unsigned kFullMask = 0xffffffffu;
 
-template <class S, bool kFull>
+template <class S, bool kFull, bool kCached>
 __device__ __forceinline__ void write_result(const TraceParams& p, int64_t q,
-                                             const Tracer<S, kFull>& T) {
+                                             const Tracer<S, kFull, kCached>& T) {
   V3<double> b = T.widened_bary();
   if (p.o_face) p.o_face[q] = T.face;
   if (p.o_bary) { p.o_bary[3 * q] = b.x; p.o_bary[3 * q + 1] = b.y; p.o_bary[3 * q + 2] = b.z; }
@@ -65,9 +65,9 @@ __device__ __forceinline__ void write_result(const TraceParams& p, int64_t q,
   }
 }
 
-template <class S, bool kFull>
+template <class S, bool kFull, bool kCached>
 __global__ void __launch_bounds__(kBlockThreads, kFull ? DG_TRACE_MIN_BLOCKS_FULL : DG_TRACE_MIN_BLOCKS) trace_kernel(const __grid_constant__ TraceParams p) {
-  Tracer<S, kFull> T(p.mesh, p.max_steps, p.hole_avoidance != 0);
+  Tracer<S, kFull, kCached> T(p.mesh, p.max_steps, p.hole_avoidance != 0);
   const unsigned lane = threadIdx.x & 31u;
   const unsigned long long n = (unsigned long long)p.n;
   bool live = false;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kBlockThreads, kFull ? DG_TRACE_MIN_BLOCKS_FUL
               T.sink.base = p.poly_offsets[q];
             }
             live = T.initialise(f, b, v, pay, has_pay, p.want_q != 0);
-            if (!live) write_result<S, kFull>(p, q, T);
+            if (!live) write_result<S, kFull, kCached>(p, q, T);
           }
         }
       }
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kBlockThreads, kFull ? DG_TRACE_MIN_BLOCKS_FUL
       live = T.run_step();
       if (!live) {
         my_crossings += (unsigned long long)T.crossings;
-        write_result<S, kFull>(p, q, T);
+        write_result<S, kFull, kCached>(p, q, T);
       }
     }
   }
@@ -128,11 +128,11 @@ __global__ void __launch_bounds__(kBlockThreads, kFull ? DG_TRACE_MIN_BLOCKS_FUL
   }
 }
 
-template <class S, bool kFull>
+template <class S, bool kFull, bool kCached>
 cudaError_t launch_one(const TraceParams& p, LaunchShape shape, cudaStream_t stream) {
   int per_sm = shape.blocks_per_sm;
   if (per_sm <= 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<S, kFull>,
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<S, kFull, kCached>,
                                                                   kBlockThreads, 0);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
@@ -141,7 +141,7 @@ cudaError_t launch_one(const TraceParams& p, LaunchShape shape, cudaStream_t str
   const long long needed = (p.n + kBlockThreads - 1) / kBlockThreads;
   if (blocks > needed) blocks = needed;
   if (blocks < 1) blocks = 1;
-  trace_kernel<S, kFull><<<unsigned(blocks), kBlockThreads, 0, stream>>>(p);
+  trace_kernel<S, kFull, kCached><<<unsigned(blocks), kBlockThreads, 0, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -151,26 +151,26 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
                          cudaStream_t stream) {
   if (p.n <= 0) return cudaSuccess;
   if (use_f32) {
-    return needs_full ? launch_one<float, true>(p, shape, stream) : launch_one<float, false>(p, shape, stream);
+    return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
-  return needs_full ? launch_one<double, true>(p, shape, stream) : launch_one<double, false>(p, shape, stream);
+  if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
+  return needs_full ? launch_one<double, true, false>(p, shape, stream) : launch_one<double, false, false>(p, shape, stream);
 }
 
-void trace_kernel_info(bool use_f32, bool full, int* regs, int* blocks_per_sm, int* block_threads) {
+void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads) {
   cudaFuncAttributes a{};
   int per_sm = 0;
-  if (use_f32 && full) {
-    cudaFuncGetAttributes(&a, trace_kernel<float, true>);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<float, true>, kBlockThreads, 0);
-  } else if (use_f32) {
-    cudaFuncGetAttributes(&a, trace_kernel<float, false>);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<float, false>, kBlockThreads, 0);
-  } else if (full) {
-    cudaFuncGetAttributes(&a, trace_kernel<double, true>);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<double, true>, kBlockThreads, 0);
+  const bool full = variant & 1, cached = (variant & 2) && !use_f32;
+  auto query = [&](auto kernel) {
+    cudaFuncGetAttributes(&a, kernel);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlockThreads, 0);
+  };
+  if (use_f32) {
+    if (full) query(trace_kernel<float, true, false>); else query(trace_kernel<float, false, false>);
+  } else if (cached) {
+    if (full) query(trace_kernel<double, true, true>); else query(trace_kernel<double, false, true>);
   } else {
-    cudaFuncGetAttributes(&a, trace_kernel<double, false>);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<double, false>, kBlockThreads, 0);
+    if (full) query(trace_kernel<double, true, false>); else query(trace_kernel<double, false, false>);
   }
   if (regs) *regs = a.numRegs;
   if (blocks_per_sm) *blocks_per_sm = per_sm;

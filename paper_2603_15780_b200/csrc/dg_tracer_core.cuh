@@ -67,7 +67,8 @@ struct PolySink {
 // kFull = payload / transport-matrix / hole-avoidance / polyline support compiled in. The lite
 // instantiation is the plain forward exp map (the benchmarked path) and carries 26 fewer live
 // f64 registers per thread.
-template <class S, bool kFull>
+// kCached = crossings read the per-half-edge transport cache (f64 only; MeshView::he != null).
+template <class S, bool kFull, bool kCached = false>
 struct Tracer {
   const MeshView& m;
   int max_steps;
@@ -293,18 +294,28 @@ struct Tracer {
       return Outcome::Boundary;
     }
     const int ka = k == 2 ? 0 : k + 1, kc = k == 0 ? 2 : k - 1;
-    const int va = cur.id(ka), vc = cur.id(kc);
     const S wa = get(bary, ka), wc = get(bary, kc);
-
-    Face<S> G = load_face<S>(m, g);
-    EdgeTransport<S> t =
-        make_edge_transport(cur.pos(ka), cur.pos(kc), cur.pos(k), G.pos_of(G.third(va, vc)));
-    dir = normalized(t(dir));
-    apply_transport(t);
-
     V3<S> nb{S(0), S(0), S(0)};
-    put(nb, G.corner_of(va), wa);
-    put(nb, G.corner_of(vc), wc);
+    Face<S> G;
+    if (kCached) {
+      // the fold isometry and the corner map of this half-edge were computed at upload
+      const HalfEdge h = load_halfedge(m, face, k);
+      G = load_face<S>(m, g);
+      EdgeTransport<S> t{cast<S>(h.edge), cast<S>(h.in_from), cast<S>(h.in_to)};
+      dir = normalized(t(dir));
+      apply_transport(t);
+      put(nb, h.ja, wa);
+      put(nb, h.jc, wc);
+    } else {
+      const int va = cur.id(ka), vc = cur.id(kc);
+      G = load_face<S>(m, g);
+      EdgeTransport<S> t =
+          make_edge_transport(cur.pos(ka), cur.pos(kc), cur.pos(k), G.pos_of(G.third(va, vc)));
+      dir = normalized(t(dir));
+      apply_transport(t);
+      put(nb, G.corner_of(va), wa);
+      put(nb, G.corner_of(vc), wc);
+    }
     face = g;
     cur = G;
     bary = nb;

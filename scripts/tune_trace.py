@@ -9,7 +9,9 @@ from bench import make_workload
 key = sys.argv[1] if len(sys.argv) > 1 else "c2"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
 xyz, tri, f, b, d, q = make_workload(key, n, 42)
-mesh = dg.Mesh(xyz, tri, device=0)
+cache = {"on": True, "off": False}.get(os.environ.get("TC", "auto"), "auto")
+mesh = dg.Mesh(xyz, tri, device=0, transport_cache=cache)
+print("transport cache:", mesh.has_transport_cache, "device MB:", mesh.device_bytes / 1e6)
 dev = torch.device("cuda", 0)
 t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt)
 F, B, D = t(f, torch.int32), t(b, torch.float64), t(d, torch.float64)

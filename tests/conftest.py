@@ -47,10 +47,10 @@ def gpu(dg):
     return dg
 
 
-def gpu_mesh(dg, rm):
+def gpu_mesh(dg, rm, transport_cache="auto"):
     """Uploads a reference-built mesh through OUR derive + create path."""
     a = rm.arrays()
-    return dg.Mesh(a["xyz"], a["tri"])
+    return dg.Mesh(a["xyz"], a["tri"], transport_cache=transport_cache)
 
 
 def assert_trace_equal(r, h, n, check_poly=True, payload=False, q=False, exact=True, tol=1e-9):

@@ -57,18 +57,21 @@ def test_icosphere_variants(gpu, ref, kw):
     assert np.array_equal(r.has_payload, h.has_payload)
 
 
-def test_torus_long_traces_bit_exact(gpu, ref):
+@pytest.mark.parametrize("cache", [True, False])
+def test_torus_long_traces_bit_exact(gpu, ref, cache):
     rm = ref.RefMesh.torus(1 / 3, 1 / 6, 200, 100)
-    m = gpu_mesh(gpu, rm)
+    m = gpu_mesh(gpu, rm, transport_cache=cache)
+    assert m.has_transport_cache == cache
     f, b, d = rm.sample_queries(7, 20000, 0.05, 1.5)
     r, h = both(rm, m, f, b, d)
     assert_trace_equal(r, h, len(f))
 
 
-def test_vertex_paths(gpu, ref):
+@pytest.mark.parametrize("cache", [True, False])
+def test_vertex_paths(gpu, ref, cache):
     """Vertex-to-vertex walks (config-5 style starts) and random departures from vertices."""
     rm = ref.RefMesh.torus(1 / 3, 1 / 6, 64, 32)
-    m = gpu_mesh(gpu, rm)
+    m = gpu_mesh(gpu, rm, transport_cache=cache)
     a = rm.arrays()
     X, T = a["xyz"], a["tri"]
     rng = np.random.default_rng(3)
@@ -261,3 +264,21 @@ def test_default_max_steps_termination_matches(gpu, ref):
     r, h = both(rm, m, f, b, d)
     assert (h.term == 2).any()
     assert_trace_equal(r, h, len(f))
+
+
+def test_transport_cache_is_bit_identical(gpu, ref):
+    """The per-half-edge transport cache (layout choice, on when it fits in L2) must not change a
+    single bit of any output: payload, Q, polylines, hole avoidance included."""
+    rng = np.random.default_rng(17)
+    for rm, seed in ((ref.RefMesh.icosphere(4), 31), (ref.RefMesh.plane(14, 11, 1.0, 3), 32)):
+        on, off = gpu_mesh(gpu, rm, True), gpu_mesh(gpu, rm, False)
+        assert on.has_transport_cache and not off.has_transport_cache
+        assert on.device_bytes > off.device_bytes
+        f, b, d = rm.sample_queries(seed, 20000, 0.05, 2.5)
+        pay = rng.normal(size=(len(f), 3))
+        for kw in (dict(), dict(payload=pay, want_q=True, hole_avoidance=True)):
+            x = on.trace_batch(f, b, d, record_polyline=True, **kw)
+            y = off.trace_batch(f, b, d, record_polyline=True, **kw)
+            for k in ("face", "bary", "dir", "traced", "term", "status", "npoints", "crossings", "poly_face",
+                      "poly_bary", "poly_seg") + (("payload", "q") if kw else ()):
+                assert np.array_equal(getattr(x, k), getattr(y, k)), k
