@@ -105,8 +105,8 @@ DG_API int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int
                           const int32_t* csr_list, dg_mesh** out);
 /* Same, with layout flags. The transport cache stores, per directed half-edge, the fold isometry
  * of tracer.cpp:113-126 (96 B per half-edge, computed on the device at upload by the same code the
- * uncached walker runs, so results are bit-identical): AUTO enables it when face records + cache
- * fit in 3/4 of the L2 (env DG_TRANSPORT_CACHE=on|off|auto overrides AUTO). */
+ * uncached walker runs, so results are bit-identical): AUTO enables it whenever the cache is
+ * at most 16 GB (env DG_TRANSPORT_CACHE=on|off overrides AUTO). */
 enum { DG_MESH_TRANSPORT_AUTO = 0, DG_MESH_TRANSPORT_ON = 1, DG_MESH_TRANSPORT_OFF = 2 };
 DG_API int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf,
                              const int32_t* adj, const double* fnormal, const double* vangle,
