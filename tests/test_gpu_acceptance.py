@@ -1,0 +1,92 @@
+"""The reference's acceptance criteria for the hot path (proj/tests/acceptance.cpp:74-201,
+SPEC.md:571-576) evaluated on the GPU path, next to the reference's own numbers for the same
+seeds: (1) sphere endpoint accuracy, (3) GFD gradient medians, (4) EP gradient behaviour,
+(5) GFD / EP cost ratio, (6) determinism with polylines across launch shapes."""
+import time
+
+import numpy as np
+import pytest
+
+from conftest import gpu_mesh
+
+pytestmark = pytest.mark.gpu
+
+
+def sphere_mean_error(m, G, samples, seed):
+    f, b, v, _ = G.draw_samples(m, samples, seed, 0.1, np.pi / 2, with_targets=False)
+    t = m.trace_batch(f, b, v)
+    p0 = m.embed(f, b)
+    ps = p0 / np.linalg.norm(p0, axis=1, keepdims=True)
+    vs = v - ps * np.einsum("nd,nd->n", v, ps)[:, None]
+    ln = np.linalg.norm(v, axis=1, keepdims=True)
+    vs = vs / np.linalg.norm(vs, axis=1, keepdims=True) * ln
+    exact = ps * np.cos(ln) + vs * (np.sin(ln) / ln)
+    return float(np.linalg.norm(m.embed(t.face, t.bary) - exact, axis=1).mean())
+
+
+def test_criterion_1_sphere_accuracy(gpu, ref):
+    from paper_2603_15780_b200 import gradcheck as G
+    e5 = sphere_mean_error(gpu_mesh(gpu, ref.RefMesh.icosphere(5)), G, 1000, 42)
+    e6 = sphere_mean_error(gpu_mesh(gpu, ref.RefMesh.icosphere(6)), G, 1000, 42)
+    assert e5 <= 5e-3 and e6 < e5
+    # the values the unmodified reference prints for the same seeds
+    assert abs(e5 - 6.10e-4) < 5e-6 and abs(e6 - 2.02e-4) < 5e-6
+
+
+@pytest.mark.parametrize("scheme", ["gfd", "ep"])
+def test_criteria_3_4_gradcheck_medians(gpu, ref, scheme):
+    from paper_2603_15780_b200 import gradcheck as G
+    rm = ref.RefMesh.icosphere(5)
+    m = gpu_mesh(gpu, rm)
+    ours = G.run_gradcheck(m, scheme, 200, 44, 0.1, np.pi / 2)
+    theirs = rm.gradcheck(scheme, 200, 44, 0.1, np.pi / 2)
+    if scheme == "gfd":
+        assert ours.median_cos_v >= 0.99 and ours.median_cos_p >= 0.99
+        assert abs(ours.median_cos_p - theirs["median_cos_p"]) < 1e-6
+        assert abs(ours.median_norm_ratio_p - theirs["median_norm_ratio_p"]) < 1e-5
+    else:
+        assert ours.median_cos_v >= 0.9 and 0.9 <= ours.median_norm_ratio_v <= 1.1
+        assert ours.max_p_grad_norm == 0.0 and theirs["max_p_grad_norm"] == 0.0
+    assert abs(ours.median_cos_v - theirs["median_cos_v"]) < 1e-6
+    assert abs(ours.median_norm_ratio_v - theirs["median_norm_ratio_v"]) < 1e-5
+
+
+def test_criterion_5_gfd_over_ep_cost_ratio(gpu, ref):
+    """Backward cost GFD / EP: the reference pins [2, 6] for (fwd + GFD) / (fwd + EP)
+    (acceptance.cpp:133-171); GFD is 4 full-length + 3 short re-traces per sample."""
+    rm = ref.RefMesh.icosphere(4)
+    m = gpu_mesh(gpu, rm)
+    f, b, v = rm.sample_queries(45, 200000, 0.1, np.pi / 2)
+    g = np.random.default_rng(0).normal(size=(len(f), 3))
+
+    def timed(fn):
+        fn()
+        t0 = time.perf_counter()
+        fn()
+        return time.perf_counter() - t0
+
+    def ep():
+        t = m.trace_batch(f, b, v)
+        m.ep_backward(f, v, t.face, t.dir, g)
+
+    def gfd():
+        m.trace_batch(f, b, v)
+        m.gfd(f, b, v, g=g)
+    ratio = timed(gfd) / timed(ep)
+    assert 1.5 <= ratio <= 8.0, ratio
+
+
+def test_criterion_6_determinism_with_polylines(gpu, ref):
+    """Bitwise identical results, polylines included, for any launch shape (the GPU analogue of
+    1 worker vs max workers, acceptance.cpp:173-201) on five fixtures x 2000 traces."""
+    fixtures = [ref.RefMesh.icosphere(3), ref.RefMesh.torus(1 / 3, 1 / 6, 48, 24), ref.RefMesh.plane(10, 10, 1.0, 3),
+                ref.RefMesh.cylinder(0.5, 1.0, 24, 6), ref.RefMesh.cone(1.0, 1.0, 16)]
+    for i, rm in enumerate(fixtures):
+        m = gpu_mesh(gpu, rm)
+        f, b, v = rm.sample_queries(50 + i, 2000, 0.05, 2.0)
+        a = m.trace_batch(f, b, v, record_polyline=True, blocks_per_sm=1)
+        c = m.trace_batch(f, b, v, record_polyline=True, refill_min=32, sort_by_face=True)
+        r = rm.trace_batch(f, b, v, record_polyline=True, workers=1)
+        for k in ("face", "bary", "dir", "traced", "term", "status", "npoints", "poly_face", "poly_bary", "poly_seg"):
+            assert np.array_equal(getattr(a, k), getattr(c, k)), k
+        assert np.array_equal(a.poly_face, r.poly_face)
