@@ -285,12 +285,15 @@ def run_ours(args):
                          npoints=pinned_empty(n, torch.int32), crossings=pinned_empty(n, torch.int32))
     hg, hgv = hq, pinned_empty((n, 3), torch.float64)   # hg: the synthetic upstream gradient
 
+    gfd_out = dict(jv=pinned_empty((n, 4), torch.float64), jp=pinned_empty((n, 4), torch.float64),
+                   degraded=pinned_empty((n, 4), torch.uint8), grad_v=hgv, grad_p=pinned_empty((n, 3), torch.float64))
+
     def e2e_step():
         r = mesh.trace_batch(hf, hb, hd, out=res)
         if scheme == "ep":
             out = mesh.ep_backward(hf, hd, r.face, r.dir, hg, grad_v=hgv)
         else:
-            out = mesh.gfd(hf, hb, hd, g=hg)
+            out = mesh.gfd(hf, hb, hd, g=hg, out=gfd_out)
         return r, out
 
     e2e_reps = max(1, min(args.steps, 3))
@@ -308,7 +311,7 @@ def run_ours(args):
     if scheme == "ep":
         h2d, d2h = fwd_in + n * (4 + 24 + 4 + 24 + 24), fwd_out + n * 24
     else:
-        h2d, d2h = fwd_in + n * (4 + 24 + 24 + 24), fwd_out + n * (32 + 32 + 4 + 264 + 24 + 24 + 4 + 24 + 24)
+        h2d, d2h = fwd_in + n * (4 + 24 + 24 + 24), fwd_out + n * (32 + 32 + 4 + 24 + 24)
 
     line = None
     if rank == 0:

@@ -255,8 +255,10 @@ class Mesh:
         check(lib().dg_ep_backward(self._handle(), int(face.numel()), ptr(face), ptr(v), ptr(end_face), ptr(end_dir),
                                    ptr(g), C.addressof(cfg), ptr(grad_v), ptr(grad_p), C.addressof(ei)), ei)
 
-    def gfd(self, face, bary, v, eps_v=None, eps_p=None, g=None, max_steps=0):
-        """gfd_batched_many (+ pullback_ambient when g is given), diff.cpp:273-326."""
+    def gfd(self, face, bary, v, eps_v=None, eps_p=None, g=None, max_steps=0, out=None):
+        """gfd_batched_many (+ pullback_ambient when g is given), diff.cpp:273-326. `out`: a dict
+        of preallocated (e.g. pinned) arrays; only the keys present are computed and copied back
+        (jv, jp, degraded, frames, grad_v, grad_p, base_face, base_bary, base_dir)."""
         h = self._handle()
         face = _i32(face)
         n = len(face)
@@ -264,16 +266,17 @@ class Mesh:
         eps = self.default_gfd_eps()
         eps_v = eps if eps_v is None else eps_v
         eps_p = eps if eps_p is None else eps_p
-        out = dict(jv=np.zeros((n, 4)), jp=np.zeros((n, 4)), degraded=np.zeros((n, 4), np.uint8),
-                   frames=np.zeros((n, capi.FRAME_DOUBLES)), grad_v=np.zeros((n, 3)), grad_p=np.zeros((n, 3)),
-                   base_face=np.empty(n, np.int32), base_bary=np.empty((n, 3)), base_dir=np.empty((n, 3)))
+        if out is None:
+            out = dict(jv=np.zeros((n, 4)), jp=np.zeros((n, 4)), degraded=np.zeros((n, 4), np.uint8),
+                       frames=np.zeros((n, capi.FRAME_DOUBLES)), grad_v=np.zeros((n, 3)), grad_p=np.zeros((n, 3)),
+                       base_face=np.empty(n, np.int32), base_bary=np.empty((n, 3)), base_dir=np.empty((n, 3)))
         ei = C.c_int64(-1)
         cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps))
+        o = lambda k: ptr(out.get(k))
         check(lib().dg_gfd_jacobians(h, n, ptr(face), ptr(bary), ptr(v), float(eps_v), float(eps_p), ptr(g),
-                                     C.addressof(cfg), ptr(out["jv"]), ptr(out["jp"]), ptr(out["degraded"]),
-                                     ptr(out["frames"]), ptr(out["grad_v"]) if g is not None else None,
-                                     ptr(out["grad_p"]) if g is not None else None, ptr(out["base_face"]),
-                                     ptr(out["base_bary"]), ptr(out["base_dir"]), C.addressof(ei)), ei)
+                                     C.addressof(cfg), o("jv"), o("jp"), o("degraded"), o("frames"),
+                                     o("grad_v") if g is not None else None, o("grad_p") if g is not None else None,
+                                     o("base_face"), o("base_bary"), o("base_dir"), C.addressof(ei)), ei)
         return out
 
     def gfd_device(self, face, bary, v, eps_v, eps_p, g, jv, jp, grad_v=None, grad_p=None, degraded=None,

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 
 #include "dg_capi_common.hpp"
 #include "dg_tracer_core.cuh"
@@ -275,6 +276,7 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
 #define DG_TRY(expr) if ((e = (expr)) != cudaSuccess) return cleanup(fail_cuda(e, #expr))
   DG_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, g_device));
   DG_TRY(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  for (auto& a : m->aux) DG_TRY(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
   {
     // Staging buffers come from the device's stream-ordered pool; keep freed blocks cached so
     // that a DG_MEM_HOST call does not pay for physical allocation on every invocation.
@@ -348,6 +350,7 @@ void dg_mesh_destroy(dg_mesh* m) {
   cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
   cudaFree(m->csr_list); cudaFree(m->vboundary); cudaFree(m->counters);
   if (m->stream) cudaStreamDestroy(m->stream);
+  for (auto& a : m->aux) if (a) cudaStreamDestroy(a);
   delete m;
 }
 
@@ -358,6 +361,77 @@ int64_t dg_mesh_device_bytes(const dg_mesh* m) { return m ? m->bytes : 0; }
 int dg_mesh_device(const dg_mesh* m) { return m ? m->device : -1; }
 
 // ------------------------------------------------------------------------- forward tracing
+
+// Enqueues one slice [lo, lo + n) of a trace request on `stream` (staging through `st`).
+static int enqueue_trace(const dg_mesh* mesh, int64_t lo, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c,
+                         const dg_trace_out* out, bool record, cudaStream_t stream, Stage& st, uint64_t* total_dst) {
+  const bool device_mode = c.memory == DG_MEM_DEVICE;
+  const size_t N = size_t(n), L = size_t(lo);
+  auto at = [L](auto* ptr, size_t stride) { return ptr ? ptr + stride * L : ptr; };
+  dg::TraceParams p{};
+  p.mesh = mesh->view();
+  p.n = n;
+  p.face = st.in(at(in->face, 1), N);
+  p.bary = st.in(at(in->bary, 3), 3 * N);
+  p.dir = st.in(at(in->dir, 3), 3 * N);
+  p.payload = st.in(at(in->payload, 3), 3 * N);
+  p.o_face = st.out(at(out->face, 1), N);
+  p.o_bary = st.out(at(out->bary, 3), 3 * N);
+  p.o_dir = st.out(at(out->dir, 3), 3 * N);
+  p.o_traced = st.out(at(out->traced, 1), N);
+  p.o_requested = st.out(at(out->requested, 1), N);
+  p.o_term = st.out(at(out->term, 1), N);
+  p.o_status = st.out(at(out->status, 1), N);
+  p.o_stall = st.out(at(out->stall, 1), N);
+  p.o_payload = st.out(at(out->payload, 3), 3 * N);
+  p.o_transport = st.out(at(out->transport, 9), 9 * N);
+  p.o_npoints = st.out(at(out->npoints, 1), N);
+  p.o_crossings = st.out(at(out->crossings, 1), N);
+  if (record) {  // never sliced: offsets index the caller's whole polyline arrays
+    const size_t T = size_t(out->poly_total);
+    p.poly_offsets = st.in(out->poly_offsets, N);
+    p.poly_face = st.out(out->poly_face, T);
+    p.poly_bary = st.out(out->poly_bary, 3 * T);
+    p.poly_seg = st.out(out->poly_seg, T);
+  }
+  p.max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
+  p.refill_min = c.refill_min ? c.refill_min : 1;
+  p.hole_avoidance = c.hole_avoidance;
+  p.want_q = c.want_transport_matrix;
+
+  unsigned long long* ctr = mesh->next_counters();
+  p.queue_head = ctr;
+  p.total_crossings = total_dst ? ctr + 1 : nullptr;
+  st.note(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), stream));
+
+  if (c.sort_by_face) {  // schedule in start-face order; results stay at the request index
+    int32_t* keys_out = st.scratch<int32_t>(N);
+    int32_t* iota = st.scratch<int32_t>(N);
+    int32_t* perm = st.scratch<int32_t>(N);
+    if (keys_out && iota && perm) {
+      iota_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(iota, n);
+      size_t tmp_bytes = 0;
+      int bits = 1;
+      while ((int64_t(1) << bits) < int64_t(mesh->nf) && bits < 31) ++bits;
+      st.note(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, p.face, keys_out, iota, perm, int(n), 0, bits, stream));
+      void* tmp = st.scratch<char>(tmp_bytes);
+      if (tmp) st.note(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, p.face, keys_out, iota, perm, int(n), 0, bits, stream));
+      p.perm = perm;
+    }
+  }
+  if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_trace_batch staging");
+
+  const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || record ||
+                          out->payload || out->transport;
+  dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm)};
+  st.note(dg::launch_trace(p, c.use_f32 != 0, needs_full, shape, stream));
+  if (total_dst) {
+    st.note(cudaMemcpyAsync(total_dst, ctr + 1, sizeof(uint64_t),
+                            device_mode ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
+  }
+  if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_trace_batch launch");
+  return DG_OK;
+}
 
 int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg,
                    dg_trace_out* out) {
@@ -388,71 +462,39 @@ int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const 
     return DG_OK;
   }
 
-  Stage st(stream, device_mode);
-  const size_t N = size_t(n);
-  dg::TraceParams p{};
-  p.mesh = mesh->view();
-  p.n = n;
-  p.face = st.in(in->face, N);
-  p.bary = st.in(in->bary, 3 * N);
-  p.dir = st.in(in->dir, 3 * N);
-  p.payload = st.in(in->payload, 3 * N);
-  p.o_face = st.out(out->face, N);
-  p.o_bary = st.out(out->bary, 3 * N);
-  p.o_dir = st.out(out->dir, 3 * N);
-  p.o_traced = st.out(out->traced, N);
-  p.o_requested = st.out(out->requested, N);
-  p.o_term = st.out(out->term, N);
-  p.o_status = st.out(out->status, N);
-  p.o_stall = st.out(out->stall, N);
-  p.o_payload = st.out(out->payload, 3 * N);
-  p.o_transport = st.out(out->transport, 9 * N);
-  p.o_npoints = st.out(out->npoints, N);
-  p.o_crossings = st.out(out->crossings, N);
-  if (record) {
-    const size_t T = size_t(out->poly_total);
-    p.poly_offsets = st.in(out->poly_offsets, N);
-    p.poly_face = st.out(out->poly_face, T);
-    p.poly_bary = st.out(out->poly_bary, 3 * T);
-    p.poly_seg = st.out(out->poly_seg, T);
+  // Host mode, large batch: split the request into up to four slices on separate streams so that
+  // the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the kernel of slice i (the
+  // persistent kernels of neighbouring slices share the SMs, so no slice pays its own tail).
+  constexpr int64_t kSliceMin = 1 << 17;
+  int slices = 1;
+  if (!device_mode && !c.stream && !record && n >= 2 * kSliceMin) slices = int(std::min<int64_t>(4, n / kSliceMin));
+  if (slices == 1) {
+    Stage st(stream, device_mode);
+    uint64_t* total_dst = out->total_crossings;
+    int rc = enqueue_trace(mesh, 0, n, in, c, out, record, stream, st, total_dst);
+    if (rc != DG_OK) return rc;
+    cudaError_t e = st.finish();
+    if (e != cudaSuccess) return fail_cuda(e, "dg_trace_batch");
+    return DG_OK;
   }
-  p.max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
-  p.refill_min = c.refill_min ? c.refill_min : 1;
-  p.hole_avoidance = c.hole_avoidance;
-  p.want_q = c.want_transport_matrix;
-
-  unsigned long long* ctr = mesh->next_counters();
-  p.queue_head = ctr;
-  p.total_crossings = out->total_crossings ? ctr + 1 : nullptr;
-  st.note(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), stream));
-
-  if (c.sort_by_face) {  // schedule in start-face order; results stay at the request index
-    int32_t* keys_out = st.scratch<int32_t>(N);
-    int32_t* iota = st.scratch<int32_t>(N);
-    int32_t* perm = st.scratch<int32_t>(N);
-    if (keys_out && iota && perm) {
-      iota_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(iota, n);
-      size_t tmp_bytes = 0;
-      int bits = 1;
-      while ((int64_t(1) << bits) < int64_t(mesh->nf) && bits < 31) ++bits;
-      st.note(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, p.face, keys_out, iota, perm, int(n), 0, bits, stream));
-      void* tmp = st.scratch<char>(tmp_bytes);
-      if (tmp) st.note(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, p.face, keys_out, iota, perm, int(n), 0, bits, stream));
-      p.perm = perm;
-    }
+  uint64_t totals[4] = {0, 0, 0, 0};
+  std::vector<std::unique_ptr<Stage>> stages;
+  int rc = DG_OK;
+  cudaError_t err = cudaSuccess;
+  for (int s = 0; s < slices && rc == DG_OK; ++s) {
+    const int64_t lo = n * s / slices, hi = n * (s + 1) / slices;
+    cudaStream_t ss = s == 0 ? mesh->stream : mesh->aux[s - 1];
+    stages.emplace_back(new Stage(ss, false));
+    rc = enqueue_trace(mesh, lo, hi - lo, in, c, out, false, ss, *stages.back(), out->total_crossings ? &totals[s] : nullptr);
+    if (rc == DG_OK) stages.back()->flush_async();
   }
-  if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_trace_batch staging");
-
-  const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || record ||
-                          out->payload || out->transport;
-  dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm)};
-  st.note(dg::launch_trace(p, c.use_f32 != 0, needs_full, shape, stream));
-  if (out->total_crossings) {
-    st.note(cudaMemcpyAsync(out->total_crossings, ctr + 1, sizeof(uint64_t),
-                            device_mode ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
+  for (size_t s = 0; s < stages.size(); ++s) {
+    cudaError_t e = cudaStreamSynchronize(s == 0 ? mesh->stream : mesh->aux[s - 1]);
+    if (err == cudaSuccess) err = e != cudaSuccess ? e : stages[s]->error();
   }
-  cudaError_t e = st.finish();
-  if (e != cudaSuccess) return fail_cuda(e, "dg_trace_batch");
+  if (rc != DG_OK) return rc;
+  if (err != cudaSuccess) return fail_cuda(err, "dg_trace_batch");
+  if (out->total_crossings) *out->total_crossings = totals[0] + totals[1] + totals[2] + totals[3];
   return DG_OK;
 }
 

@@ -28,6 +28,7 @@ struct dg_mesh {
   uint8_t* vboundary = nullptr;
   int64_t bytes = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // extra streams of the sliced host-mode pipeline
   // ring of {queue_head, total_crossings} pairs so that concurrent calls never share a cursor
   static constexpr unsigned kRing = 256;
   unsigned long long* counters = nullptr;
@@ -99,11 +100,15 @@ class Stage {
 
   // Copies the outputs back and waits (host mode); in device mode only frees scratch.
   cudaError_t finish() {
+    flush_async();
+    if (!device_mode_) note(cudaStreamSynchronize(stream_));
+    return err_;
+  }
+  // Enqueues the copies back and the frees without waiting (the caller synchronises the stream).
+  void flush_async() {
     for (auto& b : backs_) note(cudaMemcpyAsync(b.host, b.dev, b.bytes, cudaMemcpyDeviceToHost, stream_));
     backs_.clear();
     release();
-    if (!device_mode_) note(cudaStreamSynchronize(stream_));
-    return err_;
   }
   cudaError_t error() const { return err_; }
   void note(cudaError_t e) { if (err_ == cudaSuccess && e != cudaSuccess) err_ = e; }
