@@ -347,6 +347,8 @@ void dg_mesh_destroy(dg_mesh* m) {
   if (!m) return;
   DeviceGuard guard(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
+  if (m->small_pin) cudaFreeHost(m->small_pin);
+  cudaFree(m->small_dev);
   cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
   cudaFree(m->csr_list); cudaFree(m->vboundary); cudaFree(m->counters);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -361,6 +363,89 @@ int64_t dg_mesh_device_bytes(const dg_mesh* m) { return m ? m->bytes : 0; }
 int dg_mesh_device(const dg_mesh* m) { return m ? m->device : -1; }
 
 // ------------------------------------------------------------------------- forward tracing
+
+// Small host-mode batches (the opt.cpp:298-323 use: ~50 seeds per call) are launch-latency bound:
+// instead of one allocation + one copy per array, all inputs are packed into ONE pinned block
+// (one H2D), all outputs into one device block (one D2H); both blocks are kept per mesh.
+static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c,
+                       const dg_trace_out* out) {
+  const size_t N = size_t(n);
+  struct Field { const void* src; void* dst; size_t bytes; size_t off; };
+  Field fin[4] = {{in->face, nullptr, 4 * N, 0}, {in->bary, nullptr, 24 * N, 0}, {in->dir, nullptr, 24 * N, 0},
+                  {in->payload, nullptr, in->payload ? 24 * N : 0, 0}};
+  Field fout[13] = {{nullptr, out->face, out->face ? 4 * N : 0, 0},
+                    {nullptr, out->bary, out->bary ? 24 * N : 0, 0},
+                    {nullptr, out->dir, out->dir ? 24 * N : 0, 0},
+                    {nullptr, out->traced, out->traced ? 8 * N : 0, 0},
+                    {nullptr, out->requested, out->requested ? 8 * N : 0, 0},
+                    {nullptr, out->payload, out->payload ? 24 * N : 0, 0},
+                    {nullptr, out->transport, out->transport ? 72 * N : 0, 0},
+                    {nullptr, out->npoints, out->npoints ? 4 * N : 0, 0},
+                    {nullptr, out->crossings, out->crossings ? 4 * N : 0, 0},
+                    {nullptr, out->term, out->term ? N : 0, 0},
+                    {nullptr, out->status, out->status ? N : 0, 0},
+                    {nullptr, out->stall, out->stall ? N : 0, 0},
+                    {nullptr, out->total_crossings, out->total_crossings ? size_t(8) : 0, 0}};
+  auto up8 = [](size_t x) { return (x + 7) & ~size_t(7); };
+  size_t in_bytes = 16, total = 0;  // the first 16 bytes of the block are the work counters
+  for (auto& f : fin) { f.off = in_bytes; in_bytes += up8(f.bytes); }
+  total = in_bytes;
+  const size_t out_begin = total;
+  for (auto& f : fout) { f.off = total; total += up8(f.bytes); }
+
+  std::lock_guard<std::mutex> lock(mesh->small_mu);
+  if (mesh->small_cap < total) {
+    if (mesh->small_pin) cudaFreeHost(mesh->small_pin);
+    if (mesh->small_dev) cudaFree(mesh->small_dev);
+    mesh->small_pin = mesh->small_dev = nullptr;
+    mesh->small_cap = 0;
+    const size_t cap = std::max<size_t>(total * 2, size_t(1) << 16);
+    DG_CUDA(cudaMallocHost(&mesh->small_pin, cap));
+    DG_CUDA(cudaMalloc(&mesh->small_dev, cap));
+    mesh->small_cap = cap;
+  }
+  char* hp = static_cast<char*>(mesh->small_pin);
+  char* dp = static_cast<char*>(mesh->small_dev);
+  std::memset(hp, 0, 16);
+  for (auto& f : fin) if (f.bytes) std::memcpy(hp + f.off, f.src, f.bytes);
+  cudaStream_t stream = mesh->stream;
+  DG_CUDA(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, stream));
+
+  dg::TraceParams p{};
+  p.mesh = mesh->view();
+  p.n = n;
+  auto din = [&](int i) { return fin[i].bytes ? dp + fin[i].off : nullptr; };
+  auto dout = [&](int i) { return fout[i].bytes ? dp + fout[i].off : nullptr; };
+  p.face = reinterpret_cast<const int32_t*>(din(0));
+  p.bary = reinterpret_cast<const double*>(din(1));
+  p.dir = reinterpret_cast<const double*>(din(2));
+  p.payload = reinterpret_cast<const double*>(din(3));
+  p.o_face = reinterpret_cast<int32_t*>(dout(0));
+  p.o_bary = reinterpret_cast<double*>(dout(1));
+  p.o_dir = reinterpret_cast<double*>(dout(2));
+  p.o_traced = reinterpret_cast<double*>(dout(3));
+  p.o_requested = reinterpret_cast<double*>(dout(4));
+  p.o_payload = reinterpret_cast<double*>(dout(5));
+  p.o_transport = reinterpret_cast<double*>(dout(6));
+  p.o_npoints = reinterpret_cast<int32_t*>(dout(7));
+  p.o_crossings = reinterpret_cast<int32_t*>(dout(8));
+  p.o_term = reinterpret_cast<uint8_t*>(dout(9));
+  p.o_status = reinterpret_cast<uint8_t*>(dout(10));
+  p.o_stall = reinterpret_cast<uint8_t*>(dout(11));
+  p.queue_head = reinterpret_cast<unsigned long long*>(dp);
+  p.total_crossings = reinterpret_cast<unsigned long long*>(dout(12));
+  p.max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
+  p.refill_min = 1;
+  p.hole_avoidance = c.hole_avoidance;
+  p.want_q = c.want_transport_matrix;
+  if (p.total_crossings) DG_CUDA(cudaMemsetAsync(p.total_crossings, 0, 8, stream));
+  const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || out->payload || out->transport;
+  DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, needs_full, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm)}, stream));
+  if (total > out_begin) DG_CUDA(cudaMemcpyAsync(hp + out_begin, dp + out_begin, total - out_begin, cudaMemcpyDeviceToHost, stream));
+  DG_CUDA(cudaStreamSynchronize(stream));
+  for (auto& f : fout) if (f.bytes) std::memcpy(f.dst, hp + f.off, f.bytes);
+  return DG_OK;
+}
 
 // Enqueues one slice [lo, lo + n) of a trace request on `stream` (staging through `st`).
 static int enqueue_trace(const dg_mesh* mesh, int64_t lo, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c,
@@ -465,9 +550,14 @@ int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const 
   // Host mode, large batch: split the request into up to four slices on separate streams so that
   // the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the kernel of slice i (the
   // persistent kernels of neighbouring slices share the SMs, so no slice pays its own tail).
+  if (!device_mode && !c.stream && !record && !c.sort_by_face && n <= 8192) return trace_small(mesh, n, in, c, out);
   constexpr int64_t kSliceMin = 1 << 17;
   int slices = 1;
-  if (!device_mode && !c.stream && !record && n >= 2 * kSliceMin) slices = int(std::min<int64_t>(4, n / kSliceMin));
+  // measured on B200, 1 M geodesics x 207 crossings: 1 slice 13.3 ms, 2 slices 11.4 ms, 4 slices
+  // 12.0 ms (every slice pays a ~0.7 ms ramp-down), so small batches use two slices
+  if (n >= 2 * kSliceMin) slices = n >= (int64_t(1) << 22) ? 4 : 2;
+  if (const char* env = getenv("DG_TRACE_SLICES")) slices = std::max(1, std::min(4, atoi(env)));
+  if (device_mode || c.stream || record) slices = 1;
   if (slices == 1) {
     Stage st(stream, device_mode);
     uint64_t* total_dst = out->total_crossings;

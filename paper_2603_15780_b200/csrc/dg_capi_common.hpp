@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -29,6 +30,11 @@ struct dg_mesh {
   int64_t bytes = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // extra streams of the sliced host-mode pipeline
+  // small-batch path: one pinned host block + one device block, reused across calls
+  mutable std::mutex small_mu;
+  mutable void* small_pin = nullptr;
+  mutable void* small_dev = nullptr;
+  mutable size_t small_cap = 0;
   // ring of {queue_head, total_crossings} pairs so that concurrent calls never share a cursor
   static constexpr unsigned kRing = 256;
   unsigned long long* counters = nullptr;

@@ -7,6 +7,8 @@
 // number of idle lanes (warp-aggregated atomic) and every idle lane initialises the next
 // query in place. The grid is sized to the resident capacity of the chip (SM count x
 // resident blocks per SM), never to the batch.
+#include <atomic>
+
 #include "dg_kernels.cuh"
 #include "dg_tracer_core.cuh"
 
@@ -132,10 +134,15 @@ template <class S, bool kFull, bool kCached>
 cudaError_t launch_one(const TraceParams& p, LaunchShape shape, cudaStream_t stream) {
   int per_sm = shape.blocks_per_sm;
   if (per_sm <= 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<S, kFull, kCached>,
-                                                                  kBlockThreads, 0);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
+    static std::atomic<int> cached_per_sm{0};  // per kernel variant; the query costs microseconds per call
+    per_sm = cached_per_sm.load(std::memory_order_relaxed);
+    if (per_sm <= 0) {
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel<S, kFull, kCached>,
+                                                                    kBlockThreads, 0);
+      if (e != cudaSuccess) return e;
+      if (per_sm < 1) per_sm = 1;
+      cached_per_sm.store(per_sm, std::memory_order_relaxed);
+    }
   }
   long long blocks = (long long)shape.sm_count * per_sm;
   const long long needed = (p.n + kBlockThreads - 1) / kBlockThreads;
