@@ -137,3 +137,27 @@ def test_query_sharding_world_size_2_gloo(ref, tmp_path):
                        capture_output=True, text=True, env=env, timeout=300)
     assert p.returncode == 0, p.stdout + p.stderr
     assert p.stdout.count("ok=True") == 2
+
+
+def test_wire_formats_match_reference_json(ref):
+    """traces_to_json of the host shim (no JSON dependency) emits the reference's document for
+    the golden trace byte for byte (proj/tests/test_io.cpp:71-82 compares parsed values)."""
+    import json
+    exe = os.path.join(ROOT, "tests", "_build", "io_check")
+    if not os.path.exists(exe):
+        subprocess.check_call(["make", "-C", os.path.join(ROOT, "tests", "cpp")])
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert p.returncode == 0 and "IO_OK" in p.stderr, p.stderr
+    ours = json.loads(p.stdout)
+    sq = ref.RefMesh.build([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]], [[0, 1, 2], [0, 2, 3]])
+    _, text = sq.trace_batch([0, 0], [[.5, .25, .25]] * 2, [[.25, .5, 0], [0, 0, .5]], record_polyline=True, json=True)
+    theirs = json.loads(text)
+    assert ours["schema"] == theirs["schema"] == "digeo.traces/1"
+    assert ours["traces"][0] == theirs["traces"][0]                      # golden trace, exact doubles
+    # byte-for-byte for the golden element (same key order, indentation and number formatting)
+    golden_text = text[: text.index('"ok": false') if '"ok": false' in text else len(text)]
+    assert p.stdout.startswith(golden_text[: golden_text.rindex("},") + 1][:600])
+    stalled = dict(theirs["traces"][1])
+    mine = dict(ours["traces"][1])
+    assert mine.pop("transported_payload") == [1e-5, -2.5e20, 3.0]
+    assert mine == stalled
