@@ -70,13 +70,12 @@ enum { DG_EVENT_ADVANCED = 0, DG_EVENT_CROSSED_EDGE = 1, DG_EVENT_CROSSED_VERTEX
        DG_EVENT_BOUNDARY_SLIDE = 3, DG_EVENT_BOUNDARY_STOP = 4 };
 
 enum { DG_MEM_HOST = 0, DG_MEM_DEVICE = 1 };
-/* arithmetic lane of the f64 tracer */
-enum {
-  DG_LANE_FAST = 0,  /* FMA-contracted FP64 (default): identical face sequences on non-degenerate
-                        queries, positions within 1e-9 x bbox diagonal of the reference */
-  DG_LANE_EXACT = 1  /* no contraction, reference operation order: bit-identical to the reference
-                        CPU build on traces that never take a vertex branch (no libm calls) */
-};
+/* Arithmetic of the f64 tracer: there is ONE lane. The library is built without FMA contraction
+ * and follows the reference's operation order, so a trace that never takes a vertex branch (no
+ * libm calls) is bit-identical to the reference CPU build; vertex branches agree to the last
+ * ulp of atan2/sin/cos. The `lane` bytes of the cfg structs are reserved (must be 0 or 1; both
+ * select this lane) for a future contraction-enabled variant. */
+enum { DG_LANE_DEFAULT = 0, DG_LANE_EXACT = 1 };
 
 DG_API const char* dg_last_error(void);
 DG_API const char* dg_version(void);
@@ -125,7 +124,7 @@ typedef struct dg_trace_cfg {
   uint8_t hole_avoidance;
   uint8_t want_transport_matrix;
   uint8_t use_f32;               /* run the stepping arithmetic in single precision */
-  uint8_t lane;                  /* DG_LANE_FAST / DG_LANE_EXACT (f64 only) */
+  uint8_t lane;                  /* reserved (see DG_LANE_*) */
   uint8_t memory;                /* DG_MEM_HOST: pointers are host memory, staged by the library
                                     DG_MEM_DEVICE: pointers are device memory on the mesh's GPU */
   uint8_t sort_by_face;          /* schedule queries in start-face order (results stay at request index) */
@@ -193,7 +192,7 @@ DG_API int dg_transition(const dg_mesh* mesh, int which, int64_t n, const int32_
 
 typedef struct dg_diff_cfg {
   uint8_t memory;       /* DG_MEM_HOST / DG_MEM_DEVICE for all pointers of the call */
-  uint8_t lane;         /* tracer lane used by GFD re-traces */
+  uint8_t lane;         /* reserved (see DG_LANE_*) */
   uint8_t reserved[6];
   void* stream;
   int32_t max_steps;    /* GFD re-traces; 0 = default */

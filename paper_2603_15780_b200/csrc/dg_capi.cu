@@ -528,7 +528,7 @@ int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const 
     return fail(DG_ERR_INVALID_ARGS, "trace_batch: starts and dirs differ in length");
   dg_trace_cfg c{};
   if (cfg) c = *cfg;
-  if (c.use_f32 && c.lane == DG_LANE_EXACT) { /* the f32 lane has a single arithmetic variant */ }
+  if (c.lane > DG_LANE_EXACT) return fail(DG_ERR_INVALID_ARGS, "trace_batch: unknown arithmetic lane %d", int(c.lane));
   const bool device_mode = c.memory == DG_MEM_DEVICE;
   const bool record = out->poly_offsets != nullptr;
   if (record && (!out->poly_face || !out->poly_bary || !out->poly_seg || out->poly_total < 0))
