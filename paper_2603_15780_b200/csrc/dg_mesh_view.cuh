@@ -37,9 +37,23 @@ struct alignas(32) HalfEdgeRec {
 };
 static_assert(sizeof(HalfEdgeRec) == 96, "HalfEdgeRec must be three 32-byte sectors");
 
+// Optional per-face "entry record" of the fast walker (dg_fast_walk.cuh): everything advance()
+// derives from the face alone -- the two corner-0 edge vectors and their Gram matrix, exactly as
+// wedge_coeffs (tracer.cpp:130-138) computes them -- plus the neighbour ids. Built at upload by
+// the same arithmetic the generic walker runs per crossing, hence bit-identical. Word order is
+// chosen for three 256-bit loads: e1 e2.x | e2.yz g11 g12 | g22 det adj[0..2] flags.
+struct alignas(32) EntryRec {
+  double e1[3], e2[3];        // x1 - x0, x2 - x0
+  double g11, g12, g22, det;  // e1.e1, e1.e2, e2.e2, g11 g22 - g12 g12
+  int32_t adj[3];             // Mesh::face_adjacency[f]
+  int32_t flags;              // bit 0: det > 0 and every Gram entry is far from the f64 range limits
+};
+static_assert(sizeof(EntryRec) == 96, "EntryRec must be three 32-byte sectors");
+
 struct MeshView {
   const FaceRec* rec;        // [nf]
   const HalfEdgeRec* he;     // [3 nf] or null (transport cache off)
+  const EntryRec* ent;       // [nf]   or null (only with the transport cache)
   const double* fnormal;     // [3 nf] unit face normals                  (Mesh::face_normals)
   const double* vangle;      // [nv]   total interior angle per vertex    (Mesh::vertex_total_angle)
   const int32_t* csr_off;    // [nv+1] vertex -> incident faces, face order (mesh.cpp:118-127)

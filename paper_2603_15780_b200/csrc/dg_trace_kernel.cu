@@ -8,7 +8,10 @@
 // query in place. The grid is sized to the resident capacity of the chip (SM count x
 // resident blocks per SM), never to the batch.
 #include <atomic>
+#include <cstdlib>
+#include <cstring>
 
+#include "dg_fast_walk.cuh"
 #include "dg_kernels.cuh"
 #include "dg_tracer_core.cuh"
 
@@ -152,6 +155,35 @@ cudaError_t launch_one(const TraceParams& p, LaunchShape shape, cudaStream_t str
   return cudaGetLastError();
 }
 
+cudaError_t launch_fast(const TraceParams& p, LaunchShape shape, cudaStream_t stream) {
+  int per_sm = shape.blocks_per_sm;
+  if (per_sm <= 0) {
+    static std::atomic<int> cached_per_sm{0};
+    per_sm = cached_per_sm.load(std::memory_order_relaxed);
+    if (per_sm <= 0) {
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel, DG_FAST_BLOCK, 0);
+      if (e != cudaSuccess) return e;
+      if (per_sm < 1) per_sm = 1;
+      cached_per_sm.store(per_sm, std::memory_order_relaxed);
+    }
+  }
+  long long blocks = (long long)shape.sm_count * per_sm;
+  const long long needed = (p.n + DG_FAST_BLOCK - 1) / DG_FAST_BLOCK;
+  if (blocks > needed) blocks = needed;
+  if (blocks < 1) blocks = 1;
+  trace_fast_kernel<<<unsigned(blocks), DG_FAST_BLOCK, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// DG_FAST_WALK=0 keeps the generic walker on the plain f64 forward path (A/B measurements).
+bool fast_walk_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DG_FAST_WALK");
+    return !(e && (!strcmp(e, "0") || !strcmp(e, "off")));
+  }();
+  return on;
+}
+
 }  // namespace
 
 cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
@@ -160,6 +192,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
+  if (!needs_full && p.mesh.he && p.mesh.ent && fast_walk_enabled()) return launch_fast(p, shape, stream);
   if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
   return needs_full ? launch_one<double, true, false>(p, shape, stream) : launch_one<double, false, false>(p, shape, stream);
 }
@@ -175,7 +208,15 @@ void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm,
   if (use_f32) {
     if (full) query(trace_kernel<float, true, false>); else query(trace_kernel<float, false, false>);
   } else if (cached) {
-    if (full) query(trace_kernel<double, true, true>); else query(trace_kernel<double, false, true>);
+    if (full) query(trace_kernel<double, true, true>);
+    else if (fast_walk_enabled()) {
+      cudaFuncGetAttributes(&a, trace_fast_kernel);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel, DG_FAST_BLOCK, 0);
+      if (regs) *regs = a.numRegs;
+      if (blocks_per_sm) *blocks_per_sm = per_sm;
+      if (block_threads) *block_threads = DG_FAST_BLOCK;
+      return;
+    } else query(trace_kernel<double, false, true>);
   } else {
     if (full) query(trace_kernel<double, true, false>); else query(trace_kernel<double, false, false>);
   }
