@@ -78,26 +78,12 @@ __global__ void build_halfedges_kernel(const dg::MeshView m, dg::HalfEdgeRec* he
     r.t[3] = t.in_from.x; r.t[4] = t.in_from.y; r.t[5] = t.in_from.z;
     r.t[6] = t.in_to.x; r.t[7] = t.in_to.y; r.t[8] = t.in_to.z;
     r.corners = G.corner_of(va) | (G.corner_of(vc) << 2) | (G.corner_of(vt) << 4);
+    // the face-only operands of wedge_coeffs(g, 0, .), tracer.cpp:130-133
+    const V3<double> e1 = G.x1 - G.x0, e2 = G.x2 - G.x0;
+    r.e[0] = e1.x; r.e[1] = e1.y; r.e[2] = e1.z;
+    r.e[3] = e2.x; r.e[4] = e2.y; r.e[5] = e2.z;
   }
   he[s] = r;
-}
-
-// Entry records of the fast walker: the face-only part of wedge_coeffs(face, 0, .)
-// (tracer.cpp:130-138), evaluated once per face with the walker's own expression trees.
-__global__ void build_entries_kernel(const dg::MeshView m, dg::EntryRec* ent) {
-  using namespace dg;
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= m.nf) return;
-  const Face<double> c = load_face<double>(m, f);
-  const V3<double> e1 = c.x1 - c.x0, e2 = c.x2 - c.x0;
-  EntryRec r;
-  r.e1[0] = e1.x; r.e1[1] = e1.y; r.e1[2] = e1.z;
-  r.e2[0] = e2.x; r.e2[1] = e2.y; r.e2[2] = e2.z;
-  r.g11 = dot(e1, e1); r.g12 = dot(e1, e2); r.g22 = dot(e2, e2);
-  r.det = r.g11 * r.g22 - r.g12 * r.g12;
-  r.adj[0] = c.a0; r.adj[1] = c.a1; r.adj[2] = c.a2;
-  r.flags = (r.det > 0.0 && mid_range(r.det) && mid_range(r.g11) && mid_range(r.g22)) ? 1 : 0;
-  ent[f] = r;
 }
 
 __global__ void iota_kernel(int32_t* a, int64_t n) {
@@ -313,7 +299,7 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   DG_TRY(cudaMalloc(&m->vboundary, Vn));
   DG_TRY(cudaMalloc(&m->counters, 2 * dg_mesh::kRing * sizeof(unsigned long long)));
   m->bytes = int64_t(F * sizeof(dg::FaceRec) + 3 * F * 8 + Vn * 8 + (Vn + 1) * 4 + 3 * F * 4 + Vn);
-  // Transport cache policy (288 B per face on top of the 96 B face record).
+  // Transport cache policy (384 B per face on top of the 96 B face record).
   bool cache = (flags & 3u) == DG_MESH_TRANSPORT_ON;
   if ((flags & 3u) == DG_MESH_TRANSPORT_AUTO) {
     const char* env = getenv("DG_TRANSPORT_CACHE");
@@ -323,14 +309,13 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
       cache = false;
     } else {
       // Measured (profiles/tuning_r1.md): 1.29x on an L2-resident mesh (82 k faces) and still 1.04x
-      // on the 1 M-face mesh whose cache (288 MB) lives in HBM, so AUTO only guards capacity.
+      // on the 1 M-face mesh whose cache lives in HBM, so AUTO only guards capacity.
       cache = 3 * F * sizeof(dg::HalfEdgeRec) <= (size_t(16) << 30);
     }
   }
   if (cache) {
     DG_TRY(cudaMalloc(&m->he, 3 * F * sizeof(dg::HalfEdgeRec)));
-    DG_TRY(cudaMalloc(&m->ent, F * sizeof(dg::EntryRec)));
-    m->bytes += int64_t(3 * F * sizeof(dg::HalfEdgeRec) + F * sizeof(dg::EntryRec));
+    m->bytes += int64_t(3 * F * sizeof(dg::HalfEdgeRec));
   }
 
   // indexed arrays are only needed to assemble the records
@@ -345,8 +330,6 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   DG_TRY(dg::launch_build_records(d_xyz, d_tri, d_adj, nf, m->rec, m->stream));
   if (m->he) {
     build_halfedges_kernel<<<unsigned((3 * F + 127) / 128), 128, 0, m->stream>>>(m->view_uncached(), m->he);
-    DG_TRY(cudaGetLastError());
-    build_entries_kernel<<<unsigned((F + 127) / 128), 128, 0, m->stream>>>(m->view_uncached(), m->ent);
     DG_TRY(cudaGetLastError());
   }
   DG_TRY(cudaMemcpyAsync(m->fnormal, fnormal, 3 * F * sizeof(double), cudaMemcpyHostToDevice, m->stream));
@@ -370,7 +353,7 @@ void dg_mesh_destroy(dg_mesh* m) {
   if (m->stream) cudaStreamSynchronize(m->stream);
   if (m->small_pin) cudaFreeHost(m->small_pin);
   cudaFree(m->small_dev);
-  cudaFree(m->rec); cudaFree(m->he); cudaFree(m->ent); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
+  cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
   cudaFree(m->csr_list); cudaFree(m->vboundary); cudaFree(m->counters);
   if (m->stream) cudaStreamDestroy(m->stream);
   for (auto& a : m->aux) if (a) cudaStreamDestroy(a);

@@ -22,7 +22,6 @@ struct dg_mesh {
   int32_t nf = 0, nv = 0;
   dg::FaceRec* rec = nullptr;
   dg::HalfEdgeRec* he = nullptr;  // transport cache (null when off)
-  dg::EntryRec* ent = nullptr;    // entry records of the fast walker (allocated with the cache)
   double* fnormal = nullptr;
   double* vangle = nullptr;
   int32_t* csr_off = nullptr;
@@ -42,11 +41,11 @@ struct dg_mesh {
   mutable std::atomic<unsigned> ring{0};
 
   dg::MeshView view() const {
-    return dg::MeshView{rec, he, ent, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
+    return dg::MeshView{rec, he, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
   }
   // the same mesh without the transport cache (f32 lane: its transports are float arithmetic)
   dg::MeshView view_uncached() const {
-    return dg::MeshView{rec, nullptr, nullptr, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
+    return dg::MeshView{rec, nullptr, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
   }
   unsigned long long* next_counters() const { return counters + 2 * (ring.fetch_add(1) % kRing); }
 };

@@ -24,36 +24,30 @@ struct alignas(32) FaceRec {
 };
 static_assert(sizeof(FaceRec) == 96, "FaceRec must be three 32-byte sectors");
 
-// Optional per-directed-half-edge transport cache (slot 3 f + k = crossing face f through the
-// edge opposite corner k). The fold isometry of tracer.cpp:113-126 depends only on the mesh, so
-// it is computed once at upload -- by the same device functions the uncached walker runs, hence
-// bit-identical -- and a crossing becomes two gathers with no sqrt / normalisation of edge
-// frames. 80 useful bytes, padded to three 32-byte sectors.
-struct alignas(32) HalfEdgeRec {
+// Optional per-directed-half-edge crossing record (slot 3 f + k = leaving face f through the
+// edge opposite corner k): everything the walker needs to cross that edge and to take its next
+// step inside the entered face g, in ONE 128-byte line:
+//   * the fold isometry of tracer.cpp:113-126 (unit edge, in-plane edge normals of both faces).
+//     It depends only on the mesh, so it is computed once at upload -- by the same device
+//     functions the uncached walker runs, hence bit-identical -- and a crossing needs no sqrt /
+//     normalisation of edge frames;
+//   * the two corner-0 edge vectors of g, exactly as wedge_coeffs (tracer.cpp:130-138) forms them
+//     (x1 - x0, x2 - x0), which is all advance() reads of a face on the fast path;
+//   * g itself and the corner map of the shared edge in g.
+// The walk is then a chain of single-line gathers, record(3 f + k).g -> record(3 g + k').
+// The profile that led here: with 6 sectors per crossing in two records the kernel sat at 75 % of
+// the L1TEX -> crossbar request rate (one sector request per cycle per SM, profiles/).
+struct alignas(128) HalfEdgeRec {
   double t[9];      // edge, in_from, in_to (unit vectors)
+  double e[6];      // entered face: x1 - x0, x2 - x0
   int32_t g;        // face entered (-1 = boundary)
   int32_t corners;  // ja | jc << 2 | jt << 4: corners of va, vc and of the third vertex in g
-  int32_t pad[4];
 };
-static_assert(sizeof(HalfEdgeRec) == 96, "HalfEdgeRec must be three 32-byte sectors");
-
-// Optional per-face "entry record" of the fast walker (dg_fast_walk.cuh): everything advance()
-// derives from the face alone -- the two corner-0 edge vectors and their Gram matrix, exactly as
-// wedge_coeffs (tracer.cpp:130-138) computes them -- plus the neighbour ids. Built at upload by
-// the same arithmetic the generic walker runs per crossing, hence bit-identical. Word order is
-// chosen for three 256-bit loads: e1 e2.x | e2.yz g11 g12 | g22 det adj[0..2] flags.
-struct alignas(32) EntryRec {
-  double e1[3], e2[3];        // x1 - x0, x2 - x0
-  double g11, g12, g22, det;  // e1.e1, e1.e2, e2.e2, g11 g22 - g12 g12
-  int32_t adj[3];             // Mesh::face_adjacency[f]
-  int32_t flags;              // bit 0: det > 0 and every Gram entry is far from the f64 range limits
-};
-static_assert(sizeof(EntryRec) == 96, "EntryRec must be three 32-byte sectors");
+static_assert(sizeof(HalfEdgeRec) == 128, "HalfEdgeRec must be one 128-byte line");
 
 struct MeshView {
   const FaceRec* rec;        // [nf]
   const HalfEdgeRec* he;     // [3 nf] or null (transport cache off)
-  const EntryRec* ent;       // [nf]   or null (only with the transport cache)
   const double* fnormal;     // [3 nf] unit face normals                  (Mesh::face_normals)
   const double* vangle;      // [nv]   total interior angle per vertex    (Mesh::vertex_total_angle)
   const int32_t* csr_off;    // [nv+1] vertex -> incident faces, face order (mesh.cpp:118-127)
@@ -129,12 +123,13 @@ DG_HD HalfEdge load_halfedge(const MeshView& m, int f, int k) {
 #ifdef __CUDA_ARCH__
   const double2* p = reinterpret_cast<const double2*>(r);
   double2 d0 = __ldg(p + 0), d1 = __ldg(p + 1), d2 = __ldg(p + 2), d3 = __ldg(p + 3);
-  int4 w = __ldg(reinterpret_cast<const int4*>(p + 4));
+  const double t8 = __ldg(&r->t[8]);
+  const int2 w = __ldg(reinterpret_cast<const int2*>(&r->g));
   h.edge = {d0.x, d0.y, d1.x};
   h.in_from = {d1.y, d2.x, d2.y};
-  h.in_to = {d3.x, d3.y, __hiloint2double(w.y, w.x)};
-  h.g = w.z;
-  const int c = w.w;
+  h.in_to = {d3.x, d3.y, t8};
+  h.g = w.x;
+  const int c = w.y;
 #else
   h.edge = {r->t[0], r->t[1], r->t[2]};
   h.in_from = {r->t[3], r->t[4], r->t[5]};

@@ -23,7 +23,7 @@ struct HostMesh {
   std::vector<uint8_t> vboundary;
   int32_t nf, nv;
   MeshView view() const {
-    return MeshView{rec.data(), nullptr, nullptr, fnormal.data(), vangle.data(), csr_off.data(), csr_list.data(),
+    return MeshView{rec.data(), nullptr, fnormal.data(), vangle.data(), csr_off.data(), csr_list.data(),
                     vboundary.data(), nf, nv};
   }
 };
