@@ -320,7 +320,7 @@ def run_ours(args):
         alg_bytes = crossings_per_step * BYTES_PER_CROSSING + n * BYTES_PER_GEODESIC
         achieved = alg_bytes / t_trace / 1e9
         traffic = profile_traffic()
-        info = dg.kernel_info(False, False)
+        info = dg.kernel_info(False, False, cached=mesh.has_transport_cache)
         line = {"metric": f"face_crossings_per_s_fwd_{scheme}", "value": value, "unit": "face-crossings/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -332,7 +332,8 @@ def run_ours(args):
                                  "geodesics_per_s": n / t_trace},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
-                             "kernel": "trace_kernel<double,lite>", "peak_source": peak_src,
+                             "kernel": "trace_fast_kernel<cached>" if mesh.has_transport_cache else "trace_fast_kernel<uncached>",
+                             "peak_source": peak_src,
                              "algorithmic_bytes_per_launch": alg_bytes,
                              "note": "dependent-gather walk: bound by FP64 issue + L2 latency, not HBM bandwidth (DESIGN.md)",
                              "registers": info["registers"], "blocks_per_sm": info["blocks_per_sm"]},

@@ -102,10 +102,12 @@ DG_API int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int
                           const int32_t* adj, const double* fnormal, const double* vangle,
                           const uint8_t* vboundary, const int32_t* csr_off,
                           const int32_t* csr_list, dg_mesh** out);
-/* Same, with layout flags. The transport cache stores, per directed half-edge, the fold isometry
- * of tracer.cpp:113-126 (96 B per half-edge, computed on the device at upload by the same code the
- * uncached walker runs, so results are bit-identical): AUTO enables it whenever the cache is
- * at most 16 GB (env DG_TRANSPORT_CACHE=on|off overrides AUTO). */
+/* Same, with layout flags. The transport cache stores one 128-byte crossing record per directed
+ * half-edge: the fold isometry of tracer.cpp:113-126 plus the two corner-0 edge vectors of the
+ * entered face (computed on the device at upload by the same code the uncached walker runs, so
+ * results are bit-identical). AUTO enables it while the records stay within 200 MB (about 520 k
+ * faces) -- beyond that they outgrow the TLB reach and the uncached walker is faster; env
+ * DG_TRANSPORT_CACHE=on|off overrides AUTO. */
 enum { DG_MESH_TRANSPORT_AUTO = 0, DG_MESH_TRANSPORT_ON = 1, DG_MESH_TRANSPORT_OFF = 2 };
 DG_API int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf,
                              const int32_t* adj, const double* fnormal, const double* vangle,

@@ -155,13 +155,14 @@ cudaError_t launch_one(const TraceParams& p, LaunchShape shape, cudaStream_t str
   return cudaGetLastError();
 }
 
+template <bool kCached>
 cudaError_t launch_fast(const TraceParams& p, LaunchShape shape, cudaStream_t stream) {
   int per_sm = shape.blocks_per_sm;
   if (per_sm <= 0) {
     static std::atomic<int> cached_per_sm{0};
     per_sm = cached_per_sm.load(std::memory_order_relaxed);
     if (per_sm <= 0) {
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel, DG_FAST_BLOCK, 0);
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached>, DG_FAST_BLOCK, 0);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
       cached_per_sm.store(per_sm, std::memory_order_relaxed);
@@ -171,7 +172,7 @@ cudaError_t launch_fast(const TraceParams& p, LaunchShape shape, cudaStream_t st
   const long long needed = (p.n + DG_FAST_BLOCK - 1) / DG_FAST_BLOCK;
   if (blocks > needed) blocks = needed;
   if (blocks < 1) blocks = 1;
-  trace_fast_kernel<<<unsigned(blocks), DG_FAST_BLOCK, 0, stream>>>(p);
+  trace_fast_kernel<kCached><<<unsigned(blocks), DG_FAST_BLOCK, 0, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -192,37 +193,33 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
-  if (!needs_full && p.mesh.he && fast_walk_enabled()) return launch_fast(p, shape, stream);
+  if (!needs_full && fast_walk_enabled())
+    return p.mesh.he ? launch_fast<true>(p, shape, stream) : launch_fast<false>(p, shape, stream);
   if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
   return needs_full ? launch_one<double, true, false>(p, shape, stream) : launch_one<double, false, false>(p, shape, stream);
 }
 
 void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads) {
   cudaFuncAttributes a{};
-  int per_sm = 0;
+  int per_sm = 0, threads = kBlockThreads;
   const bool full = variant & 1, cached = (variant & 2) && !use_f32;
-  auto query = [&](auto kernel) {
+  auto query = [&](auto kernel, int block) {
     cudaFuncGetAttributes(&a, kernel);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlockThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
+    threads = block;
   };
   if (use_f32) {
-    if (full) query(trace_kernel<float, true, false>); else query(trace_kernel<float, false, false>);
+    if (full) query(trace_kernel<float, true, false>, kBlockThreads); else query(trace_kernel<float, false, false>, kBlockThreads);
+  } else if (!full && fast_walk_enabled()) {
+    if (cached) query(trace_fast_kernel<true>, DG_FAST_BLOCK); else query(trace_fast_kernel<false>, DG_FAST_BLOCK);
   } else if (cached) {
-    if (full) query(trace_kernel<double, true, true>);
-    else if (fast_walk_enabled()) {
-      cudaFuncGetAttributes(&a, trace_fast_kernel);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel, DG_FAST_BLOCK, 0);
-      if (regs) *regs = a.numRegs;
-      if (blocks_per_sm) *blocks_per_sm = per_sm;
-      if (block_threads) *block_threads = DG_FAST_BLOCK;
-      return;
-    } else query(trace_kernel<double, false, true>);
+    if (full) query(trace_kernel<double, true, true>, kBlockThreads); else query(trace_kernel<double, false, true>, kBlockThreads);
   } else {
-    if (full) query(trace_kernel<double, true, false>); else query(trace_kernel<double, false, false>);
+    if (full) query(trace_kernel<double, true, false>, kBlockThreads); else query(trace_kernel<double, false, false>, kBlockThreads);
   }
   if (regs) *regs = a.numRegs;
   if (blocks_per_sm) *blocks_per_sm = per_sm;
-  if (block_threads) *block_threads = kBlockThreads;
+  if (block_threads) *block_threads = threads;
 }
 
 }  // namespace dg
