@@ -288,12 +288,18 @@ def run_ours(args):
     gfd_out = dict(jv=pinned_empty((n, 4), torch.float64), jp=pinned_empty((n, 4), torch.float64),
                    degraded=pinned_empty((n, 4), torch.uint8), grad_v=hgv, grad_p=pinned_empty((n, 3), torch.float64))
 
+    # the host-facing call of a training step: a resident batch (dg_batch_*), i.e. the forward inputs and
+    # results stay on the GPU between the forward and the backward call; every step still copies its
+    # inputs host -> device and every result device -> host
+    batch = dg.Batch(mesh, n)
+    gfd_keys = dict(jv=gfd_out["jv"], jp=gfd_out["jp"], degraded=gfd_out["degraded"], grad_v=hgv, grad_p=gfd_out["grad_p"])
+
     def e2e_step():
-        r = mesh.trace_batch(hf, hb, hd, out=res)
+        r = batch.trace(hf, hb, hd, out=res)
         if scheme == "ep":
-            out = mesh.ep_backward(hf, hd, r.face, r.dir, hg, grad_v=hgv)
+            out = batch.ep_backward(hg, grad_v=hgv)
         else:
-            out = mesh.gfd(hf, hb, hd, g=hg, out=gfd_out)
+            out = batch.gfd(g=hg, out=gfd_keys)
         return r, out
 
     e2e_reps = max(1, min(args.steps, 3))
@@ -309,9 +315,9 @@ def run_ours(args):
     e2e_value = crossings_all / (float(e2e_ms.item()) * 1e-3)
     fwd_in, fwd_out = n * (4 + 24 + 24), n * (4 + 24 + 24 + 8 + 8 + 1 + 1 + 1 + 4 + 4)
     if scheme == "ep":
-        h2d, d2h = fwd_in + n * (4 + 24 + 4 + 24 + 24), fwd_out + n * 24
+        h2d, d2h = fwd_in + n * 24, fwd_out + n * 24                       # + g in, grad_v out
     else:
-        h2d, d2h = fwd_in + n * (4 + 24 + 24 + 24), fwd_out + n * (32 + 32 + 4 + 24 + 24)
+        h2d, d2h = fwd_in + n * 24, fwd_out + n * (32 + 32 + 4 + 24 + 24)  # + g in; jv, jp, degraded, grad_v, grad_p out
 
     line = None
     if rank == 0:

@@ -17,6 +17,8 @@
  *   dg_gfd_jacobians      <- gfd_batched_many / gfd_batched / gfd_jacobian_v/p
  *                                                              proj/src/diff.cpp:208-326
  *   dg_pullback           <- pullback / pullback_ambient       proj/src/diff.cpp:328-354
+ *   dg_batch_*            <- the call pair trace_batch -> EP loop / gfd_batched_many of one
+ *                            training step                        proj/src/gradcheck.cpp:70-89
  *
  * All functions return DG_OK (0) or a DG_ERR_* code, never throw and never abort;
  * dg_last_error() gives the message of the last failure on the calling thread.
@@ -228,6 +230,29 @@ DG_API int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face,
                             uint8_t* degraded, double* frames, double* grad_v, double* grad_p,
                             int32_t* base_face, double* base_bary, double* base_dir,
                             int64_t* err_index);
+
+/* ---- resident batch (forward + backward on the same samples) --------------------------------
+ * A training step runs trace_batch (tracer.hpp:94) and then the EP loop ep_jacobians +
+ * pullback_ambient (gradcheck.cpp:76-89) or gfd_batched_many (gradcheck.cpp:74) on the SAME
+ * samples. A dg_batch keeps the forward inputs and results of that step on the GPU between the
+ * two calls, so the backward moves only the upstream gradient in and the gradients out. All
+ * pointers are HOST pointers (pinned memory lets the copies overlap the kernels); the arithmetic
+ * is that of dg_trace_batch / dg_ep_backward / dg_gfd_jacobians, bit for bit. */
+typedef struct dg_batch dg_batch;
+DG_API int dg_batch_create(const dg_mesh* mesh, int64_t capacity, dg_batch** out);
+DG_API void dg_batch_destroy(dg_batch* b);
+DG_API int64_t dg_batch_size(const dg_batch* b);
+/* Plain forward exp map (no payload / transport matrix / hole avoidance / polylines: those go
+ * through dg_trace_batch). cfg->memory must be DG_MEM_HOST and cfg->stream NULL. */
+DG_API int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg,
+                          dg_trace_out* out);
+/* EP backward of the resident samples: g [3n] in, grad_v [3n] (and grad_p [3n], zero) out. */
+DG_API int dg_batch_ep_backward(dg_batch* b, const double* g, double* grad_v, double* grad_p,
+                                int64_t* err_index);
+/* GFD Jacobians (+ pull-back when g is given) of the resident samples; outputs may be NULL. */
+DG_API int dg_batch_gfd(dg_batch* b, double eps_v, double eps_p, const double* g, int32_t max_steps,
+                        double* jv, double* jp, uint8_t* degraded, double* grad_v, double* grad_p,
+                        int64_t* err_index);
 
 #ifdef __cplusplus
 }

@@ -4,9 +4,9 @@ Python surface over libdigeo_b200.so (hand-written sm_100a CUDA behind a C-ABI).
 package loads the shared library and raises if it has not been built: there is no CPU path.
 """
 from . import capi
-from .api import Mesh, TraceResult, kernel_info
+from .api import Batch, Mesh, TraceResult, kernel_info
 from .capi import DgError, device_count
 
 capi.lib()  # fail loudly at import time when the native library is absent
 
-__all__ = ["Mesh", "TraceResult", "DgError", "device_count", "kernel_info", "capi"]
+__all__ = ["Batch", "Mesh", "TraceResult", "DgError", "device_count", "kernel_info", "capi"]

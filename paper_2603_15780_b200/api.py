@@ -290,6 +290,75 @@ class Mesh:
                                      ptr(grad_v), ptr(grad_p), None, None, None, C.addressof(ei)), ei)
 
 
+class Batch:
+    """Resident batch (dg_batch_*): forward exp map, then EP or GFD backward on the same samples,
+    with the forward state kept on the GPU between the calls. Host arrays in, host arrays out."""
+
+    def __init__(self, mesh, capacity):
+        self.mesh = mesh
+        self.capacity = int(capacity)
+        h = C.c_void_p()
+        check(lib().dg_batch_create(mesh._handle(), self.capacity, C.addressof(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dg_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the library handle may already be gone
+            pass
+
+    def trace(self, face, bary, dirs, max_steps=0, refill_min=0, blocks_per_sm=0, out=None):
+        face, bary, dirs = _i32(face), _f64(bary), _f64(dirs)
+        n = len(face)
+        if bary.size != 3 * n or dirs.size != 3 * n:
+            raise DgError(1, "trace_batch: starts and dirs differ in length")
+        r = out if out is not None else TraceResult(
+            face=np.empty(n, np.int32), bary=np.empty((n, 3)), dir=np.empty((n, 3)),
+            traced=np.empty(n), requested=np.empty(n), term=np.empty(n, np.uint8),
+            status=np.empty(n, np.uint8), stall=np.empty(n, np.uint8),
+            npoints=np.empty(n, np.int32), crossings=np.empty(n, np.int32))
+        cfg = TraceCfg(max_steps=int(max_steps), memory=capi.MEM_HOST, refill_min=int(refill_min),
+                       blocks_per_sm=int(blocks_per_sm))
+        tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), None)
+        total = C.c_uint64(0)
+        o = TraceOut(ptr(r.face), ptr(r.bary), ptr(r.dir), ptr(r.traced), ptr(r.requested), ptr(r.term),
+                     ptr(r.status), ptr(r.stall), None, None, ptr(r.npoints), ptr(r.crossings),
+                     C.addressof(total), None, 0, None, None, None)
+        check(lib().dg_batch_trace(self._h, n, C.addressof(tin), C.addressof(cfg), C.addressof(o)))
+        r.total_crossings = int(total.value)
+        return r
+
+    def ep_backward(self, g, grad_v=None, grad_p=None):
+        n = int(lib().dg_batch_size(self._h))
+        g = _f64(g)
+        if grad_v is None:
+            grad_v = np.empty((n, 3))
+        ei = C.c_int64(-1)
+        check(lib().dg_batch_ep_backward(self._h, ptr(g), ptr(grad_v), ptr(grad_p), C.addressof(ei)), ei)
+        return grad_v
+
+    def gfd(self, eps_v=None, eps_p=None, g=None, max_steps=0, out=None):
+        n = int(lib().dg_batch_size(self._h))
+        g = _f64(g)
+        eps = self.mesh.default_gfd_eps()
+        eps_v = eps if eps_v is None else eps_v
+        eps_p = eps if eps_p is None else eps_p
+        if out is None:
+            out = dict(jv=np.zeros((n, 4)), jp=np.zeros((n, 4)), degraded=np.zeros((n, 4), np.uint8),
+                       grad_v=np.zeros((n, 3)), grad_p=np.zeros((n, 3)))
+        ei = C.c_int64(-1)
+        o = lambda k: ptr(out.get(k))
+        check(lib().dg_batch_gfd(self._h, float(eps_v), float(eps_p), ptr(g), int(max_steps), o("jv"), o("jp"),
+                                 o("degraded"), o("grad_v") if g is not None else None,
+                                 o("grad_p") if g is not None else None, C.addressof(ei)), ei)
+        return out
+
+
 def kernel_info(use_f32=False, full=False, cached=False):
     regs, bps, bt = C.c_int(0), C.c_int(0), C.c_int(0)
     lib().dg_trace_kernel_info(int(use_f32), int(full) | (int(cached) << 1), C.addressof(regs), C.addressof(bps),

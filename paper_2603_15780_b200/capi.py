@@ -38,6 +38,7 @@ EXPORTS = [
     "dg_mesh_derive", "dg_mesh_create", "dg_mesh_create_ex", "dg_mesh_has_transport_cache", "dg_mesh_destroy", "dg_mesh_face_count", "dg_mesh_vertex_count",
     "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_transition", "dg_ep_jacobians",
     "dg_ep_backward", "dg_gfd_jacobians", "dg_trace_kernel_info",
+    "dg_batch_create", "dg_batch_destroy", "dg_batch_size", "dg_batch_trace", "dg_batch_ep_backward", "dg_batch_gfd",
 ]
 
 
@@ -104,6 +105,14 @@ def lib():
         L.dg_gfd_jacobians.argtypes = [vp, i64, vp, vp, vp, dbl, dbl] + [vp] * 12
         L.dg_trace_kernel_info.argtypes = [C.c_int, C.c_int, vp, vp, vp]
         L.dg_trace_kernel_info.restype = None
+        L.dg_batch_create.argtypes = [vp, i64, vp]
+        L.dg_batch_destroy.argtypes = [vp]
+        L.dg_batch_destroy.restype = None
+        L.dg_batch_size.argtypes = [vp]
+        L.dg_batch_size.restype = i64
+        L.dg_batch_trace.argtypes = [vp, i64, vp, vp, vp]
+        L.dg_batch_ep_backward.argtypes = [vp] * 5
+        L.dg_batch_gfd.argtypes = [vp, dbl, dbl, vp, i32] + [vp] * 6
         _lib = L
     return _lib
 

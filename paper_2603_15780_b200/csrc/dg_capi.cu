@@ -354,6 +354,7 @@ void dg_mesh_destroy(dg_mesh* m) {
   if (!m) return;
   DeviceGuard guard(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
+  if (m->host_batch) dg_batch_destroy(m->host_batch);
   if (m->small_pin) cudaFreeHost(m->small_pin);
   cudaFree(m->small_dev);
   cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
@@ -554,44 +555,32 @@ int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const 
     return DG_OK;
   }
 
-  // Host mode, large batch: split the request into up to four slices on separate streams so that
-  // the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the kernel of slice i (the
-  // persistent kernels of neighbouring slices share the SMs, so no slice pays its own tail).
   if (!device_mode && !c.stream && !record && !c.sort_by_face && n <= 8192) return trace_small(mesh, n, in, c, out);
-  constexpr int64_t kSliceMin = 1 << 17;
-  int slices = 1;
-  // measured on B200, 1 M geodesics x 207 crossings: 1 slice 13.3 ms, 2 slices 11.4 ms, 4 slices
-  // 12.0 ms (every slice pays a ~0.7 ms ramp-down), so small batches use two slices
-  if (n >= 2 * kSliceMin) slices = n >= (int64_t(1) << 22) ? 4 : 2;
-  if (const char* env = getenv("DG_TRACE_SLICES")) slices = std::max(1, std::min(4, atoi(env)));
-  if (device_mode || c.stream || record) slices = 1;
-  if (slices == 1) {
-    Stage st(stream, device_mode);
-    uint64_t* total_dst = out->total_crossings;
-    int rc = enqueue_trace(mesh, 0, n, in, c, out, record, stream, st, total_dst);
-    if (rc != DG_OK) return rc;
-    cudaError_t e = st.finish();
-    if (e != cudaSuccess) return fail_cuda(e, "dg_trace_batch");
-    return DG_OK;
+
+  // Host mode, large plain batch: the copy/compute pipeline of the resident batch (slices on
+  // separate streams: the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the walker
+  // of slice i) over device buffers the mesh keeps between calls. Measured on B200, 1 M geodesics
+  // x 207 crossings, walker 4.0 ms: single stream 6.4 ms, pipeline 5.1 ms (stream-ordered
+  // allocations per slice serialise the streams and give 6.3-6.8 ms, which is why the buffers persist).
+  const bool plain = !in->payload && !out->payload && !out->transport && !c.want_transport_matrix && !c.hole_avoidance;
+  if (!device_mode && !c.stream && !record && plain && n >= (int64_t(1) << 16)) {
+    std::lock_guard<std::mutex> lock(mesh->host_batch_mu);
+    if (!mesh->host_batch || mesh->host_batch_cap < n) {
+      if (mesh->host_batch) dg_batch_destroy(mesh->host_batch);
+      mesh->host_batch = nullptr;
+      mesh->host_batch_cap = 0;
+      int rc = dg_batch_create(mesh, n, &mesh->host_batch);
+      if (rc != DG_OK) return rc;
+      mesh->host_batch_cap = n;
+    }
+    return dg_batch_trace(mesh->host_batch, n, in, &c, out);
   }
-  uint64_t totals[4] = {0, 0, 0, 0};
-  std::vector<std::unique_ptr<Stage>> stages;
-  int rc = DG_OK;
-  cudaError_t err = cudaSuccess;
-  for (int s = 0; s < slices && rc == DG_OK; ++s) {
-    const int64_t lo = n * s / slices, hi = n * (s + 1) / slices;
-    cudaStream_t ss = s == 0 ? mesh->stream : mesh->aux[s - 1];
-    stages.emplace_back(new Stage(ss, false));
-    rc = enqueue_trace(mesh, lo, hi - lo, in, c, out, false, ss, *stages.back(), out->total_crossings ? &totals[s] : nullptr);
-    if (rc == DG_OK) stages.back()->flush_async();
-  }
-  for (size_t s = 0; s < stages.size(); ++s) {
-    cudaError_t e = cudaStreamSynchronize(s == 0 ? mesh->stream : mesh->aux[s - 1]);
-    if (err == cudaSuccess) err = e != cudaSuccess ? e : stages[s]->error();
-  }
+
+  Stage st(stream, device_mode);
+  int rc = enqueue_trace(mesh, 0, n, in, c, out, record, stream, st, out->total_crossings);
   if (rc != DG_OK) return rc;
-  if (err != cudaSuccess) return fail_cuda(err, "dg_trace_batch");
-  if (out->total_crossings) *out->total_crossings = totals[0] + totals[1] + totals[2] + totals[3];
+  cudaError_t e = st.finish();
+  if (e != cudaSuccess) return fail_cuda(e, "dg_trace_batch");
   return DG_OK;
 }
 

@@ -1,0 +1,236 @@
+// Resident batch: the query batch of a training step (forward exp map, then EP or GFD backward)
+// kept on the GPU between the two calls, so that the backward only moves the upstream gradient in
+// and the gradients out. It replaces the call pair trace_batch (tracer.hpp:94) -> ep_jacobians +
+// pullback_ambient loop / gfd_batched_many (gradcheck.cpp:70-89) when both run on the same
+// samples. Host pointers in, host pointers out; the arithmetic is the device-mode path of
+// dg_trace_batch / dg_ep_backward / dg_gfd_jacobians, so results are bit-identical to those calls.
+#include <algorithm>
+
+#include "dg_capi_common.hpp"
+
+using namespace dgapi;
+
+struct dg_batch {
+  const dg_mesh* mesh = nullptr;
+  int device = 0;  // copy: dg_batch_destroy must not look at the mesh (it may already be gone)
+  int64_t cap = 0, n = 0;
+  bool traced = false;
+  static constexpr int kStreams = 8;
+  cudaStream_t streams[kStreams] = {};
+  // forward inputs and results
+  int32_t *face = nullptr, *o_face = nullptr, *o_npoints = nullptr, *o_crossings = nullptr;
+  double *bary = nullptr, *dir = nullptr, *o_bary = nullptr, *o_dir = nullptr, *o_traced = nullptr, *o_requested = nullptr;
+  uint8_t *o_term = nullptr, *o_status = nullptr, *o_stall = nullptr;
+  uint64_t* totals = nullptr;  // [kStreams] per-slice crossing counts
+  // backward
+  double *g = nullptr, *grad_v = nullptr, *grad_p = nullptr, *jv = nullptr, *jp = nullptr;
+  uint8_t* degraded = nullptr;
+};
+
+namespace {
+
+template <class T>
+cudaError_t dev_alloc(T** p, size_t count) { return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)); }
+
+int slices_for(int64_t n) {
+  if (const char* env = getenv("DG_BATCH_SLICES")) return std::max(1, std::min(dg_batch::kStreams, atoi(env)));
+  if (n >= (int64_t(1) << 18)) return 4;
+  if (n >= (int64_t(1) << 16)) return 2;
+  return 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dg_batch_create(const dg_mesh* mesh, int64_t capacity, dg_batch** out) {
+  if (!out) return fail(DG_ERR_INVALID_ARGS, "dg_batch_create: null output handle");
+  *out = nullptr;
+  if (!mesh) return fail(DG_ERR_INVALID_ARGS, "dg_batch_create: missing mesh");
+  if (capacity <= 0 || capacity > 0x7fffffffLL / 4) return fail(DG_ERR_INVALID_ARGS, "dg_batch_create: capacity out of range");
+  DeviceGuard guard(mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
+  dg_batch* b = new dg_batch;
+  b->mesh = mesh;
+  b->device = mesh->device;
+  b->cap = capacity;
+  const size_t N = size_t(capacity);
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  for (auto& s : b->streams) ok(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  ok(dev_alloc(&b->face, N)); ok(dev_alloc(&b->bary, 3 * N)); ok(dev_alloc(&b->dir, 3 * N));
+  ok(dev_alloc(&b->o_face, N)); ok(dev_alloc(&b->o_bary, 3 * N)); ok(dev_alloc(&b->o_dir, 3 * N));
+  ok(dev_alloc(&b->o_traced, N)); ok(dev_alloc(&b->o_requested, N));
+  ok(dev_alloc(&b->o_term, N)); ok(dev_alloc(&b->o_status, N)); ok(dev_alloc(&b->o_stall, N));
+  ok(dev_alloc(&b->o_npoints, N)); ok(dev_alloc(&b->o_crossings, N));
+  ok(dev_alloc(&b->totals, size_t(dg_batch::kStreams)));
+  ok(dev_alloc(&b->g, 3 * N)); ok(dev_alloc(&b->grad_v, 3 * N)); ok(dev_alloc(&b->grad_p, 3 * N));
+  if (e != cudaSuccess) {
+    dg_batch_destroy(b);
+    return fail_cuda(e, "dg_batch_create");
+  }
+  *out = b;
+  return DG_OK;
+}
+
+void dg_batch_destroy(dg_batch* b) {
+  if (!b) return;
+  DeviceGuard guard(b->device);
+  for (auto& s : b->streams) if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+  cudaFree(b->face); cudaFree(b->bary); cudaFree(b->dir); cudaFree(b->o_face); cudaFree(b->o_bary); cudaFree(b->o_dir);
+  cudaFree(b->o_traced); cudaFree(b->o_requested); cudaFree(b->o_term); cudaFree(b->o_status); cudaFree(b->o_stall);
+  cudaFree(b->o_npoints); cudaFree(b->o_crossings); cudaFree(b->totals);
+  cudaFree(b->g); cudaFree(b->grad_v); cudaFree(b->grad_p); cudaFree(b->jv); cudaFree(b->jp); cudaFree(b->degraded);
+  delete b;
+}
+
+int64_t dg_batch_size(const dg_batch* b) { return b && b->traced ? b->n : 0; }
+
+// Forward exp map of n host-resident queries. The request is cut into slices on separate streams:
+// the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the walker of slice i.
+int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, dg_trace_out* out) {
+  if (!b) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace: missing batch");
+  if (n < 0 || n > b->cap) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace: batch size exceeds the capacity");
+  if (!in || !out) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace: null request or result block");
+  if (n > 0 && (!in->face || !in->bary || !in->dir))
+    return fail(DG_ERR_INVALID_ARGS, "trace_batch: starts and dirs differ in length");
+  dg_trace_cfg c{};
+  if (cfg) c = *cfg;
+  if (in->payload || out->payload || out->transport || out->poly_offsets || c.want_transport_matrix || c.hole_avoidance)
+    return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace: payload / transport matrix / hole avoidance / polylines go through dg_trace_batch");
+  if (c.memory != DG_MEM_HOST || c.stream) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace: host pointers, library streams");
+  DeviceGuard guard(b->mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
+  b->traced = false;
+  b->n = n;
+  if (n == 0) {
+    if (out->total_crossings) *out->total_crossings = 0;
+    b->traced = true;
+    return DG_OK;
+  }
+  const int S = slices_for(n);
+  cudaError_t e = cudaSuccess;
+  auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  int rc = DG_OK;
+  for (int s = 0; s < S && rc == DG_OK; ++s) {
+    const int64_t lo = n * s / S, m = n * (s + 1) / S - lo;
+    const size_t L = size_t(lo), M = size_t(m);
+    cudaStream_t st = b->streams[s];
+    note(cudaMemcpyAsync(b->face + L, in->face + L, M * 4, cudaMemcpyHostToDevice, st));
+    note(cudaMemcpyAsync(b->bary + 3 * L, in->bary + 3 * L, M * 24, cudaMemcpyHostToDevice, st));
+    note(cudaMemcpyAsync(b->dir + 3 * L, in->dir + 3 * L, M * 24, cudaMemcpyHostToDevice, st));
+    dg_trace_in din{b->face + L, b->bary + 3 * L, b->dir + 3 * L, nullptr};
+    dg_trace_out dout{};
+    dout.face = b->o_face + L; dout.bary = b->o_bary + 3 * L; dout.dir = b->o_dir + 3 * L;
+    dout.traced = b->o_traced + L; dout.requested = b->o_requested + L;
+    dout.term = b->o_term + L; dout.status = b->o_status + L; dout.stall = b->o_stall + L;
+    dout.npoints = out->npoints ? b->o_npoints + L : nullptr;
+    dout.crossings = out->crossings ? b->o_crossings + L : nullptr;
+    dout.total_crossings = b->totals + s;
+    dg_trace_cfg dc = c;
+    dc.memory = DG_MEM_DEVICE;
+    dc.stream = st;
+    // One resident CTA slot per SM is left to the neighbouring slice, so that its walker ramps up
+    // while this one drains (measured, 1 M geodesics: 4 slices x 4 CTAs/SM 5.8 ms, x 3 CTAs/SM 5.1 ms).
+    if (S > 1 && dc.blocks_per_sm == 0) dc.blocks_per_sm = 3;
+    rc = dg_trace_batch(b->mesh, m, &din, &dc, &dout);
+    if (rc != DG_OK) break;
+    auto back = [&](auto* host, const auto* dev, size_t stride) {
+      if (host) note(cudaMemcpyAsync(host + stride * L, dev + stride * L, M * stride * sizeof(*host), cudaMemcpyDeviceToHost, st));
+    };
+    back(out->face, b->o_face, 1); back(out->bary, b->o_bary, 3); back(out->dir, b->o_dir, 3);
+    back(out->traced, b->o_traced, 1); back(out->requested, b->o_requested, 1);
+    back(out->term, b->o_term, 1); back(out->status, b->o_status, 1); back(out->stall, b->o_stall, 1);
+    back(out->npoints, b->o_npoints, 1); back(out->crossings, b->o_crossings, 1);
+  }
+  uint64_t totals[dg_batch::kStreams] = {};
+  for (int s = 0; s < S; ++s) {
+    if (rc == DG_OK && out->total_crossings)
+      note(cudaMemcpyAsync(&totals[s], b->totals + s, sizeof(uint64_t), cudaMemcpyDeviceToHost, b->streams[s]));
+    note(cudaStreamSynchronize(b->streams[s]));
+  }
+  if (rc != DG_OK) return rc;
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_trace");
+  if (out->total_crossings) {
+    uint64_t t = 0;
+    for (int s = 0; s < S; ++s) t += totals[s];
+    *out->total_crossings = t;
+  }
+  b->traced = true;
+  return DG_OK;
+}
+
+// EP backward (diff.cpp:44-66, 328-354) on the resident samples: g in, grad_v (and grad_p) out.
+int dg_batch_ep_backward(dg_batch* b, const double* g, double* grad_v, double* grad_p, int64_t* err_index) {
+  if (err_index) *err_index = -1;
+  if (!b || !b->traced) return fail(DG_ERR_INVALID_ARGS, "dg_batch_ep_backward: no traced batch is resident");
+  const int64_t n = b->n;
+  if (n == 0) return DG_OK;
+  if (!g || !grad_v) return fail(DG_ERR_INVALID_ARGS, "dg_ep_backward: null argument");
+  DeviceGuard guard(b->mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
+  const int S = slices_for(n);
+  cudaError_t e = cudaSuccess;
+  auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  for (int s = 0; s < S; ++s) {  // all uploads are in flight before the first kernel is waited for
+    const size_t L = size_t(n * s / S), M = size_t(n * (s + 1) / S) - L;
+    note(cudaMemcpyAsync(b->g + 3 * L, g + 3 * L, M * 24, cudaMemcpyHostToDevice, b->streams[s]));
+  }
+  int rc = DG_OK;
+  for (int s = 0; s < S && rc == DG_OK; ++s) {
+    const size_t L = size_t(n * s / S), M = size_t(n * (s + 1) / S) - L;
+    dg_diff_cfg dc{};
+    dc.memory = DG_MEM_DEVICE;
+    dc.stream = b->streams[s];
+    int64_t idx = -1;
+    rc = dg_ep_backward(b->mesh, int64_t(M), b->face + L, b->dir + 3 * L, b->o_face + L, b->o_dir + 3 * L, b->g + 3 * L,
+                        &dc, b->grad_v + 3 * L, grad_p ? b->grad_p + 3 * L : nullptr, &idx);
+    if (rc != DG_OK) {
+      if (err_index && idx >= 0) *err_index = idx + int64_t(L);
+      break;
+    }
+    note(cudaMemcpyAsync(grad_v + 3 * L, b->grad_v + 3 * L, M * 24, cudaMemcpyDeviceToHost, b->streams[s]));
+    if (grad_p) note(cudaMemcpyAsync(grad_p + 3 * L, b->grad_p + 3 * L, M * 24, cudaMemcpyDeviceToHost, b->streams[s]));
+  }
+  for (int s = 0; s < S; ++s) note(cudaStreamSynchronize(b->streams[s]));
+  if (rc != DG_OK) return rc;
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_ep_backward");
+  return DG_OK;
+}
+
+// GFD backward (diff.cpp:273-326) on the resident samples.
+int dg_batch_gfd(dg_batch* b, double eps_v, double eps_p, const double* g, int32_t max_steps, double* jv, double* jp,
+                 uint8_t* degraded, double* grad_v, double* grad_p, int64_t* err_index) {
+  if (err_index) *err_index = -1;
+  if (!b || !b->traced) return fail(DG_ERR_INVALID_ARGS, "dg_batch_gfd: no traced batch is resident");
+  const int64_t n = b->n;
+  if (n == 0) return DG_OK;
+  DeviceGuard guard(b->mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
+  const size_t N = size_t(n), C = size_t(b->cap);
+  cudaError_t e = cudaSuccess;
+  auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  if (!b->jv) { note(dev_alloc(&b->jv, 4 * C)); note(dev_alloc(&b->jp, 4 * C)); note(dev_alloc(&b->degraded, 4 * C)); }
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_gfd");
+  cudaStream_t st = b->streams[0];
+  if (g) note(cudaMemcpyAsync(b->g, g, N * 24, cudaMemcpyHostToDevice, st));
+  dg_diff_cfg dc{};
+  dc.memory = DG_MEM_DEVICE;
+  dc.stream = st;
+  dc.max_steps = max_steps;
+  const bool pull = g != nullptr;
+  int rc = dg_gfd_jacobians(b->mesh, n, b->face, b->bary, b->dir, eps_v, eps_p, pull ? b->g : nullptr, &dc, b->jv, b->jp,
+                            b->degraded, nullptr, pull && grad_v ? b->grad_v : nullptr, pull && grad_p ? b->grad_p : nullptr,
+                            nullptr, nullptr, nullptr, err_index);
+  if (rc != DG_OK) return rc;
+  if (jv) note(cudaMemcpyAsync(jv, b->jv, N * 32, cudaMemcpyDeviceToHost, st));
+  if (jp) note(cudaMemcpyAsync(jp, b->jp, N * 32, cudaMemcpyDeviceToHost, st));
+  if (degraded) note(cudaMemcpyAsync(degraded, b->degraded, N * 4, cudaMemcpyDeviceToHost, st));
+  if (pull && grad_v) note(cudaMemcpyAsync(grad_v, b->grad_v, N * 24, cudaMemcpyDeviceToHost, st));
+  if (pull && grad_p) note(cudaMemcpyAsync(grad_p, b->grad_p, N * 24, cudaMemcpyDeviceToHost, st));
+  note(cudaStreamSynchronize(st));
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_gfd");
+  return DG_OK;
+}
+
+}  // extern "C"

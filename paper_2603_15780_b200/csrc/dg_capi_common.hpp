@@ -16,6 +16,8 @@
 #include "../../include/dg_b200.h"
 #include "dg_kernels.cuh"
 
+struct dg_batch;
+
 struct dg_mesh {
   int device = 0;
   int sm_count = 0;
@@ -35,6 +37,10 @@ struct dg_mesh {
   mutable void* small_pin = nullptr;
   mutable void* small_dev = nullptr;
   mutable size_t small_cap = 0;
+  // large plain host-mode batches run through a resident batch (dg_capi_batch.cu) owned by the mesh
+  mutable std::mutex host_batch_mu;
+  mutable struct dg_batch* host_batch = nullptr;
+  mutable int64_t host_batch_cap = 0;
   // ring of {queue_head, total_crossings} pairs so that concurrent calls never share a cursor
   static constexpr unsigned kRing = 256;
   unsigned long long* counters = nullptr;

@@ -1,0 +1,78 @@
+"""Resident batch (dg_batch_*): forward + EP / GFD backward on device-resident samples.
+Bar: the same bits as the separate host-mode calls (it runs their device-mode paths), and parity
+with the UNMODIFIED reference on the forward results and the EP gradient; every slice count of
+the copy/compute pipeline gives the same bits."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import assert_trace_equal, gpu_mesh
+
+pytestmark = pytest.mark.gpu
+
+
+def unit_rows(rng, n):
+    q = rng.normal(size=(n, 3))
+    return q / np.linalg.norm(q, axis=1, keepdims=True)
+
+
+@pytest.mark.parametrize("slices", ["1", "2", "4"])
+def test_batch_forward_ep_matches_reference_and_separate_calls(gpu, ref, slices, monkeypatch):
+    monkeypatch.setenv("DG_BATCH_SLICES", slices)
+    rm = ref.RefMesh.icosphere(4)
+    m = gpu_mesh(gpu, rm)
+    n = 20011
+    f, b, d = rm.sample_queries(7, n, 0.2, 1.5)
+    batch = gpu.Batch(m, n + 5)
+    h = batch.trace(f, b, d)
+    r = rm.trace_batch(f, b, d, record_polyline=True)  # the reference counts points only when it records them
+    assert_trace_equal(r, h, n, check_poly=False)
+    h2 = m.trace_batch(f, b, d)
+    for k in ("face", "bary", "dir", "traced", "requested", "term", "status", "stall", "npoints", "crossings"):
+        assert np.array_equal(getattr(h, k), getattr(h2, k)), k
+    assert h.total_crossings == h2.total_crossings == int(h2.crossings.sum())
+    g = 2.0 * (m.embed(h.face, h.bary) - unit_rows(np.random.default_rng(1), n))  # gradcheck.cpp:88
+    gp = np.full((n, 3), np.nan)
+    gv = batch.ep_backward(g, grad_p=gp)
+    theirs = rm.ep(f, b, d, h.face, h.bary, h.dir, g=g)
+    assert np.array_equal(gv, theirs["grad_v"]) and not gp.any()
+    assert np.array_equal(gv, m.ep_backward(f, d, h.face, h.dir, g))
+
+
+def test_batch_gfd_matches_separate_call(gpu, ref):
+    rm = ref.RefMesh.torus(1 / 3, 1 / 6, 64, 32)
+    m = gpu_mesh(gpu, rm)
+    n = 3000
+    f, b, d = rm.sample_queries(11, n, 0.05, 0.4)
+    batch = gpu.Batch(m, n)
+    h = batch.trace(f, b, d)
+    g = unit_rows(np.random.default_rng(2), n)
+    ours = batch.gfd(g=g)
+    sep = m.gfd(f, b, d, g=g)
+    for k in ("jv", "jp", "degraded", "grad_v", "grad_p"):
+        assert np.array_equal(ours[k], sep[k]), k
+    theirs = rm.gfd(f, b, d, g=g)
+    scale = np.abs(theirs["jv"]).max()
+    assert np.abs(ours["jv"] - theirs["jv"]).max() <= 1e-5 * scale  # SURVEY.md 8c tolerance
+
+
+def test_batch_contract_errors(gpu, ref):
+    rm = ref.RefMesh.icosphere(2)
+    m = gpu_mesh(gpu, rm)
+    batch = gpu.Batch(m, 16)
+    with pytest.raises(gpu.DgError) as e:
+        batch.ep_backward(np.zeros((4, 3)))
+    assert e.value.klass == "InvalidArgs"
+    f, b, d = rm.sample_queries(3, 32, 1.0, 1.0)
+    with pytest.raises(gpu.DgError) as e:
+        batch.trace(f, b, d)  # exceeds the capacity
+    assert e.value.klass == "InvalidArgs"
+    h = batch.trace(f[:16], b[:16], d[:16])
+    d0 = d[:16].copy()
+    d0[5] = 0.0
+    h = batch.trace(f[:16], b[:16], d0)  # zero-length request: a valid trace, a degenerate EP direction
+    assert h.traced[5] == 0.0
+    with pytest.raises(gpu.DgError) as e:
+        batch.ep_backward(np.ones((16, 3)))
+    assert e.value.klass == "DegenerateDirection" and e.value.index == 5
