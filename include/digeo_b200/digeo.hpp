@@ -22,6 +22,8 @@
 #include <utility>
 #include <vector>
 
+struct dg_batch;  // include/dg_b200.h
+
 namespace digeo {
 
 // ---- geometry.hpp ------------------------------------------------------------------------
@@ -237,6 +239,35 @@ TraceSoA trace_batch_soa(const Mesh& m, std::span<const int32_t> face, std::span
                          std::span<const double> dir, std::span<const double> payload, const TraceConfig& cfg);
 
 // ---- diff.hpp ----------------------------------------------------------------------------
+struct GfdConfig;
+
+// One training step on device-resident samples (dg_batch_*): the forward exp map, then the EP or
+// GFD backward of the SAME samples, without sending the forward state back to the GPU. Replaces
+// the call pair trace_batch -> ep_jacobians/pullback_ambient loop | gfd_batched_many of
+// gradcheck.cpp:70-89; results are bit-identical to those calls.
+class ResidentBatch {
+ public:
+  ResidentBatch(const Mesh& m, size_t capacity);
+  ~ResidentBatch();
+  ResidentBatch(const ResidentBatch&) = delete;
+  ResidentBatch& operator=(const ResidentBatch&) = delete;
+  // plain forward exp map (cfg: max_steps / use_f32 only)
+  TraceSoA trace(std::span<const int32_t> face, std::span<const double> bary, std::span<const double> dir,
+                 const TraceConfig& cfg = {});
+  // grad_v [3n] of pullback_ambient(g_i, ep_jacobians(sample_i)); grad_p is identically zero
+  std::vector<double> ep_backward(std::span<const double> g);
+  struct Gfd {
+    std::vector<double> jv, jp;       // [4n] row-major 2x2 per sample
+    std::vector<uint8_t> degraded;    // [4n] degraded_v[0..1], degraded_p[0..1]
+    std::vector<double> grad_v, grad_p;  // [3n], filled when g is given
+  };
+  Gfd gfd(const GfdConfig& cfg, std::span<const double> g = {});
+  size_t size() const;
+
+ private:
+  ::dg_batch* h_ = nullptr;
+};
+
 struct TangentFrame {
   SurfacePoint origin;
   Vec3d e_par, e_perp, normal;

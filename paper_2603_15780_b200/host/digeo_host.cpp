@@ -403,6 +403,50 @@ TraceSoA trace_batch_soa(const Mesh& m, std::span<const int32_t> face, std::span
   return r;
 }
 
+// resident batch ------------------------------------------------------------------------
+ResidentBatch::ResidentBatch(const Mesh& m, size_t capacity) {
+  check(dg_batch_create(m.device().handle(), int64_t(capacity), &h_));
+}
+ResidentBatch::~ResidentBatch() { dg_batch_destroy(h_); }
+size_t ResidentBatch::size() const { return size_t(dg_batch_size(h_)); }
+
+TraceSoA ResidentBatch::trace(std::span<const int32_t> face, std::span<const double> bary, std::span<const double> dir,
+                              const TraceConfig& cfg) {
+  const size_t n = face.size();
+  if (bary.size() != 3 * n || dir.size() != 3 * n) throw InvalidArgs("trace_batch: starts and dirs differ in length");
+  TraceSoA r;
+  r.face.resize(n); r.bary.resize(3 * n); r.dir.resize(3 * n); r.traced.resize(n); r.requested.resize(n);
+  r.term.resize(n); r.status.resize(n); r.stall.resize(n); r.crossings.resize(n);
+  dg_trace_cfg k = to_cfg(cfg);
+  dg_trace_in in{face.data(), bary.data(), dir.data(), nullptr};
+  dg_trace_out o{};
+  o.face = r.face.data(); o.bary = r.bary.data(); o.dir = r.dir.data(); o.traced = r.traced.data();
+  o.requested = r.requested.data(); o.term = r.term.data(); o.status = r.status.data(); o.stall = r.stall.data();
+  o.crossings = r.crossings.data(); o.total_crossings = &r.total_crossings;
+  check(dg_batch_trace(h_, int64_t(n), &in, &k, &o));
+  return r;
+}
+
+std::vector<double> ResidentBatch::ep_backward(std::span<const double> g) {
+  const size_t n = size();
+  if (g.size() != 3 * n) throw InvalidArgs("ep_backward: one upstream gradient per resident sample");
+  std::vector<double> grad_v(3 * n);
+  check(dg_batch_ep_backward(h_, g.data(), grad_v.data(), nullptr, nullptr));
+  return grad_v;
+}
+
+ResidentBatch::Gfd ResidentBatch::gfd(const GfdConfig& cfg, std::span<const double> g) {
+  const size_t n = size();
+  if (!g.empty() && g.size() != 3 * n) throw InvalidArgs("gfd: one upstream gradient per resident sample");
+  Gfd r;
+  r.jv.resize(4 * n); r.jp.resize(4 * n); r.degraded.resize(4 * n);
+  if (!g.empty()) { r.grad_v.resize(3 * n); r.grad_p.resize(3 * n); }
+  check(dg_batch_gfd(h_, cfg.eps_v, cfg.eps_p, g.empty() ? nullptr : g.data(), 0, r.jv.data(), r.jp.data(),
+                     r.degraded.data(), g.empty() ? nullptr : r.grad_v.data(), g.empty() ? nullptr : r.grad_p.data(),
+                     nullptr));
+  return r;
+}
+
 // single transitions --------------------------------------------------------------------
 namespace {
 struct Transition {

@@ -267,6 +267,29 @@ static void test_differentials() {
     CHECK((one.j_v - gfd[i].j_v).max_abs() == 0 && (one.j_p - gfd[i].j_p).max_abs() == 0);
     CHECK(gfd_jacobian_v(ico, samples[i].p, samples[i].v, traces[i], default_gfd_config(ico)).a == gfd[i].j_v.a);
   }
+  // resident batch: forward + EP / GFD backward on device-resident samples, same bits as the calls above
+  {
+    const size_t n = samples.size();
+    std::vector<int32_t> face(n);
+    std::vector<double> bary(3 * n), dir(3 * n), gs(3 * n);
+    for (size_t i = 0; i < n; ++i) {
+      face[i] = samples[i].p.face;
+      for (int k = 0; k < 3; ++k) { bary[3 * i + k] = samples[i].p.bary[k]; dir[3 * i + k] = samples[i].v[k]; gs[3 * i + k] = g[i][k]; }
+    }
+    ResidentBatch rb(ico, n);
+    TraceSoA fwd = rb.trace(face, bary, dir);
+    CHECK(rb.size() == n);
+    std::vector<double> rgv = rb.ep_backward(gs);
+    ResidentBatch::Gfd rg = rb.gfd(default_gfd_config(ico), gs);
+    for (size_t i = 0; i < n; ++i) {
+      CHECK(fwd.face[i] == traces[i].final_point.face && fwd.bary[3 * i + 1] == traces[i].final_point.bary.y);
+      CHECK(Vec3d(rgv[3 * i], rgv[3 * i + 1], rgv[3 * i + 2]) == gv[i]);
+      CHECK(rg.jv[4 * i] == gfd[i].j_v.a && rg.jp[4 * i + 3] == gfd[i].j_p.d);
+      PulledGradients pf = pullback_ambient(g[i], gfd[i]);
+      CHECK(near(Vec3d(rg.grad_v[3 * i], rg.grad_v[3 * i + 1], rg.grad_v[3 * i + 2]), pf.grad_v, 1e-12));
+    }
+    CHECK(throws<InvalidArgs>([&] { rb.ep_backward(std::vector<double>(3)); }));
+  }
   CHECK(throws<DegenerateDirection>([&] { ep_jacobians(ico, samples[0].p, {0, 0, 0}, traces[0]); }));
   CHECK(throws<DegenerateDirection>([&] { make_tangent_frame(ico, samples[0].p, ico.face_normals[samples[0].p.face]); }));
   // GFD whole-call failure when a base trace leaves the mesh (diff.cpp:121-124)
