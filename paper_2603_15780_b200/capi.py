@@ -54,7 +54,8 @@ class DgError(RuntimeError):
 class TraceCfg(C.Structure):
     _fields_ = [("max_steps", C.c_int32), ("hole_avoidance", C.c_uint8), ("want_transport_matrix", C.c_uint8),
                 ("use_f32", C.c_uint8), ("lane", C.c_uint8), ("memory", C.c_uint8), ("sort_by_face", C.c_uint8),
-                ("refill_min", C.c_uint8), ("blocks_per_sm", C.c_uint8), ("stream", C.c_void_p)]
+                ("refill_min", C.c_uint8), ("blocks_per_sm", C.c_uint8), ("walker", C.c_uint8),
+                ("reserved", C.c_uint8 * 3), ("stream", C.c_void_p)]
 
 
 class TraceIn(C.Structure):

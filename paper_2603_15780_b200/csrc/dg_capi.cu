@@ -448,7 +448,7 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   p.want_q = c.want_transport_matrix;
   if (p.total_crossings) DG_CUDA(cudaMemsetAsync(p.total_crossings, 0, 8, stream));
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || out->payload || out->transport;
-  DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, needs_full, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm)}, stream));
+  DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, needs_full, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm), c.walker == DG_WALKER_GENERIC}, stream));
   if (total > out_begin) DG_CUDA(cudaMemcpyAsync(hp + out_begin, dp + out_begin, total - out_begin, cudaMemcpyDeviceToHost, stream));
   DG_CUDA(cudaStreamSynchronize(stream));
   for (auto& f : fout) if (f.bytes) std::memcpy(f.dst, hp + f.off, f.bytes);
@@ -516,7 +516,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t lo, int64_t n, const dg_tr
 
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || record ||
                           out->payload || out->transport;
-  dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm)};
+  dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm), c.walker == DG_WALKER_GENERIC};
   st.note(dg::launch_trace(p, c.use_f32 != 0, needs_full, shape, stream));
   if (total_dst) {
     st.note(cudaMemcpyAsync(total_dst, ctr + 1, sizeof(uint64_t),

@@ -46,6 +46,7 @@ struct TraceParams {
 struct LaunchShape {
   int sm_count;
   int blocks_per_sm;  // 0 = use the occupancy query
+  bool generic = false;  // never take the fast walker (cross-checks, measurements)
 };
 
 // needs_full: any of payload / transport matrix / hole avoidance / polyline is requested.

@@ -193,7 +193,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
-  if (!needs_full && fast_walk_enabled())
+  if (!needs_full && !shape.generic && fast_walk_enabled())
     return p.mesh.he ? launch_fast<true>(p, shape, stream) : launch_fast<false>(p, shape, stream);
   if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
   return needs_full ? launch_one<double, true, false>(p, shape, stream) : launch_one<double, false, false>(p, shape, stream);

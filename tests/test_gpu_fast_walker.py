@@ -1,0 +1,100 @@
+"""The fast walker (csrc/dg_fast_walk.cuh) against the general state machine it shortcuts
+(csrc/dg_tracer_core.cuh, i.e. proj/src/tracer.cpp:44-529), through the C-ABI with the walker
+selector of dg_trace_cfg. Bar: EVERY output bit-identical -- faces, barycentrics, directions,
+lengths, termination / status / stall bytes, crossing and point counts -- on every mesh family,
+both mesh layouts, and on the inputs that exercise each exit from the fast path: vertex hits,
+boundaries, step limits, exact zeros, rejected starts, zero-length requests."""
+import numpy as np
+import pytest
+
+from paper_2603_15780_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("face", "bary", "dir", "traced", "requested", "term", "status", "stall", "npoints", "crossings")
+
+
+def both_walkers(m, f, b, d, **kw):
+    fast = m.trace_batch(f, b, d, **kw)
+    slow = m.trace_batch(f, b, d, generic_walker=True, **kw)
+    for k in FIELDS:
+        x, y = getattr(fast, k), getattr(slow, k)
+        same = (x == y) | ((x != x) & (y != y))
+        bad = np.nonzero(~same.reshape(len(f), -1).all(1))[0]
+        assert len(bad) == 0, f"{k}: {len(bad)}/{len(f)} differ, first {bad[:5]}: fast {x[bad[:3]]} generic {y[bad[:3]]}"
+    assert fast.total_crossings == slow.total_crossings == int(slow.crossings.sum())
+    return fast
+
+
+@pytest.mark.parametrize("cache", [True, False])
+def test_bumpy_sphere_config2_style(gpu, cache):
+    xyz, tri = W.bumpy_sphere(5)
+    m = gpu.Mesh(xyz, tri, transport_cache=cache)
+    assert m.has_transport_cache == cache
+    f, b, d = W.sample_queries(xyz, tri, 150_000, 0.5 * W.bbox_diagonal(xyz), seed=3)
+    r = both_walkers(m, f, b, d)
+    assert (r.term == 0).all() and (r.status == 0).all() and np.abs(r.traced - r.requested).max() < 1e-9
+
+
+@pytest.mark.parametrize("cache", [True, False])
+def test_noisy_torus_mixed_lengths_and_step_limit(gpu, cache):
+    xyz, tri = W.torus(1 / 3, 1 / 6, 300, 150, noise=0.1, seed=7)
+    m = gpu.Mesh(xyz, tri, transport_cache=cache)
+    n = 60_000
+    diag = W.bbox_diagonal(xyz)
+    f, b, d = W.sample_queries(xyz, tri, n, (1e-4 * diag, 2.0 * diag), seed=9)  # log-uniform lengths: divergence stress
+    both_walkers(m, f, b, d)
+    r = both_walkers(m, f, b, d, max_steps=37)  # MaxSteps terminations leave through the generic funnel
+    assert (r.term == 2).any() and (r.term == 0).any()
+
+
+@pytest.mark.parametrize("cache", [True, False])
+def test_vertex_to_vertex_walks(gpu, cache):
+    xyz, tri = W.torus(1 / 3, 1 / 6, 64, 32)
+    m = gpu.Mesh(xyz, tri, transport_cache=cache)
+    f, b, d = W.vertex_edge_queries(xyz, tri, 4000, 1.0, seed=5)
+    f2, b2, d2 = W.sample_queries(xyz, tri, 4000, 1.0, seed=6)
+    both_walkers(m, np.concatenate([f, f2]), np.concatenate([b, b2]), np.concatenate([d, d2]))
+
+
+@pytest.mark.parametrize("cache", [True, False])
+def test_flat_grid_exact_zeros_and_boundary(gpu, ref, cache):
+    """Axis-aligned directions on a planar grid: zero numerators in every quotient, vertex hits,
+    edge-tangent slides and boundary stops."""
+    rm = ref.RefMesh.plane(12, 12, 1.0, 0)
+    a = rm.arrays()
+    m = gpu.Mesh(a["xyz"], a["tri"], transport_cache=cache)
+    f, b, d = rm.sample_queries(21, 6000, 0.05, 3.0)
+    d[:1500] = np.array([1.0, 0.0, 0.0]) * np.linalg.norm(d[:1500], axis=1, keepdims=True)
+    d[1500:3000] = np.array([0.0, -1.0, 0.0]) * np.linalg.norm(d[1500:3000], axis=1, keepdims=True)
+    b[3000:3300] = np.array([0.5, 0.5, 0.0])       # starts on an edge
+    b[3300:3600] = np.array([0.0, 0.0, 1.0])       # starts at a vertex
+    r = both_walkers(m, f, b, d)
+    assert (r.term == 1).any()                      # some leave through the boundary
+    ours = m.trace_batch(f, b, d, record_polyline=True)
+    theirs = rm.trace_batch(f, b, d, record_polyline=True)
+    assert np.array_equal(ours.face, theirs.face) and np.array_equal(ours.poly_face, theirs.poly_face)
+    # bit-equal to the reference wherever no vertex branch (libm atan2 / sincos) was taken
+    no_vertex = np.ones(len(f), bool)
+    at_vertex = (theirs.poly_bary == 1.0).any(1)
+    np.logical_and.at(no_vertex, np.repeat(np.arange(len(f)), np.diff(theirs.poly_offsets)), ~at_vertex)
+    assert no_vertex.sum() > 3000
+    assert np.array_equal(r.face, theirs.face)
+    assert np.array_equal(r.bary[no_vertex], theirs.bary[no_vertex]) and np.array_equal(r.dir[no_vertex], theirs.dir[no_vertex])
+    assert np.abs(r.bary - theirs.bary).max() < 1e-9 and np.abs(r.dir - theirs.dir).max() < 1e-9
+
+
+def test_rejected_and_degenerate_starts(gpu):
+    xyz, tri = W.icosphere(3)
+    m = gpu.Mesh(xyz, tri)
+    f, b, d = W.sample_queries(xyz, tri, 2000, 1.0, seed=1)
+    f[10] = -1; f[11] = len(tri)                   # face out of range
+    b[20] = [0.7, 0.7, 0.7]                        # not in the simplex
+    d[30] = 0.0                                    # zero-length request
+    n = np.cross(xyz[tri[f[40], 1]] - xyz[tri[f[40], 0]], xyz[tri[f[40], 2]] - xyz[tri[f[40], 0]])
+    d[40] = n / np.linalg.norm(n)                  # normal to the anchor face
+    d[50] *= 1e-300                                # tiny but positive length
+    b[60] = [np.nan, 0.5, 0.5]
+    d[70] = [np.nan, 0.0, 1.0]
+    r = both_walkers(m, f, b, d)
+    assert list(r.stall[[10, 11, 20, 40]]) == [4, 4, 5, 3] and r.traced[30] == 0.0
