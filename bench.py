@@ -226,7 +226,8 @@ def run_ours(args):
             e0.record()
             mesh.trace_batch_device(F, B, D, o)
             e1.record()
-            mesh.gfd_device(F, B, D, eps, eps, G, jv, jp, grad_v, grad_p)
+            # the forward results are GFD's base traces (the `trace` argument of gfd_batched, diff.hpp:73)
+            mesh.gfd_device(F, B, D, eps, eps, G, jv, jp, grad_v, grad_p, base=o)
             launches = 1 + 3 + 3 + 1  # fwd + (jobs, lite, payload) + (jobs, lite, assemble) ... see DESIGN.md
         if world > 1:   # results gathered over NVLink; no reduction on this path
             pack[:, 0] = o["face"].double(); pack[:, 1:4] = o["bary"]; pack[:, 4:7] = o["dir"]

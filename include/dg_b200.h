@@ -236,6 +236,21 @@ DG_API int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face,
                             int32_t* base_face, double* base_bary, double* base_dir,
                             int64_t* err_index);
 
+/* The same with the base traces given -- the forward results (final face / barycentrics /
+ * direction, termination and status bytes) of the same samples, as gfd_batched, gfd_jacobian_v and
+ * gfd_jacobian_p take them (diff.hpp:63-73: the `trace` argument): only the four perturbed traces
+ * per sample run. The caller guarantees the base traces were produced by dg_trace_batch on
+ * (face, bary, v) in f64 with the step limit of cfg->max_steps; results are then bit-identical to
+ * dg_gfd_jacobians. */
+DG_API int dg_gfd_jacobians_with_base(const dg_mesh* mesh, int64_t n, const int32_t* face,
+                                      const double* bary, const double* v, const int32_t* base_face,
+                                      const double* base_bary, const double* base_dir,
+                                      const uint8_t* base_term, const uint8_t* base_status,
+                                      double eps_v, double eps_p, const double* g,
+                                      const dg_diff_cfg* cfg, double* jv, double* jp,
+                                      uint8_t* degraded, double* frames, double* grad_v,
+                                      double* grad_p, int64_t* err_index);
+
 /* ---- resident batch (forward + backward on the same samples) --------------------------------
  * A training step runs trace_batch (tracer.hpp:94) and then the EP loop ep_jacobians +
  * pullback_ambient (gradcheck.cpp:76-89) or gfd_batched_many (gradcheck.cpp:74) on the SAME

@@ -257,7 +257,7 @@ class Mesh:
         check(lib().dg_ep_backward(self._handle(), int(face.numel()), ptr(face), ptr(v), ptr(end_face), ptr(end_dir),
                                    ptr(g), C.addressof(cfg), ptr(grad_v), ptr(grad_p), C.addressof(ei)), ei)
 
-    def gfd(self, face, bary, v, eps_v=None, eps_p=None, g=None, max_steps=0, out=None):
+    def gfd(self, face, bary, v, eps_v=None, eps_p=None, g=None, max_steps=0, out=None, base=None):
         """gfd_batched_many (+ pullback_ambient when g is given), diff.cpp:273-326. `out`: a dict
         of preallocated (e.g. pinned) arrays; only the keys present are computed and copied back
         (jv, jp, degraded, frames, grad_v, grad_p, base_face, base_bary, base_dir)."""
@@ -275,6 +275,13 @@ class Mesh:
         ei = C.c_int64(-1)
         cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps))
         o = lambda k: ptr(out.get(k))
+        if base is not None:  # a TraceResult of trace_batch on the same samples (gfd_batched's `trace` argument)
+            check(lib().dg_gfd_jacobians_with_base(
+                h, n, ptr(face), ptr(bary), ptr(v), ptr(_i32(base.face)), ptr(_f64(base.bary)), ptr(_f64(base.dir)),
+                ptr(base.term), ptr(base.status), float(eps_v), float(eps_p), ptr(g), C.addressof(cfg), o("jv"), o("jp"),
+                o("degraded"), o("frames"), o("grad_v") if g is not None else None,
+                o("grad_p") if g is not None else None, C.addressof(ei)), ei)
+            return out
         check(lib().dg_gfd_jacobians(h, n, ptr(face), ptr(bary), ptr(v), float(eps_v), float(eps_p), ptr(g),
                                      C.addressof(cfg), o("jv"), o("jp"), o("degraded"), o("frames"),
                                      o("grad_v") if g is not None else None, o("grad_p") if g is not None else None,
@@ -282,11 +289,20 @@ class Mesh:
         return out
 
     def gfd_device(self, face, bary, v, eps_v, eps_p, g, jv, jp, grad_v=None, grad_p=None, degraded=None,
-                   stream=None, max_steps=0):
+                   stream=None, max_steps=0, base=None):
+        """`base`: the forward results of the same samples (dict of device tensors face / bary / dir /
+        term / status, as trace_batch_device writes them): GFD then takes them as its base traces
+        (the `trace` argument of gfd_batched, diff.hpp:73) instead of re-tracing them."""
         import torch
         cfg = DiffCfg(memory=capi.MEM_DEVICE, max_steps=int(max_steps),
                       stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
         ei = C.c_int64(-1)
+        if base is not None:
+            check(lib().dg_gfd_jacobians_with_base(
+                self._handle(), int(face.numel()), ptr(face), ptr(bary), ptr(v), ptr(base["face"]), ptr(base["bary"]),
+                ptr(base["dir"]), ptr(base["term"]), ptr(base["status"]), float(eps_v), float(eps_p), ptr(g),
+                C.addressof(cfg), ptr(jv), ptr(jp), ptr(degraded), None, ptr(grad_v), ptr(grad_p), C.addressof(ei)), ei)
+            return
         check(lib().dg_gfd_jacobians(self._handle(), int(face.numel()), ptr(face), ptr(bary), ptr(v), float(eps_v),
                                      float(eps_p), ptr(g), C.addressof(cfg), ptr(jv), ptr(jp), ptr(degraded), None,
                                      ptr(grad_v), ptr(grad_p), None, None, None, C.addressof(ei)), ei)

@@ -5,7 +5,6 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
-#include <memory>
 
 #include "dg_capi_common.hpp"
 #include "dg_tracer_core.cuh"
@@ -280,7 +279,6 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
 #define DG_TRY(expr) if ((e = (expr)) != cudaSuccess) return cleanup(fail_cuda(e, #expr))
   DG_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, g_device));
   DG_TRY(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
-  for (auto& a : m->aux) DG_TRY(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
   {
     // Staging buffers come from the device's stream-ordered pool; keep freed blocks cached so
     // that a DG_MEM_HOST call does not pay for physical allocation on every invocation.
@@ -360,7 +358,6 @@ void dg_mesh_destroy(dg_mesh* m) {
   cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
   cudaFree(m->csr_list); cudaFree(m->vboundary); cudaFree(m->counters);
   if (m->stream) cudaStreamDestroy(m->stream);
-  for (auto& a : m->aux) if (a) cudaStreamDestroy(a);
   delete m;
 }
 
@@ -455,12 +452,12 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   return DG_OK;
 }
 
-// Enqueues one slice [lo, lo + n) of a trace request on `stream` (staging through `st`).
-static int enqueue_trace(const dg_mesh* mesh, int64_t lo, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c,
+// Enqueues a trace request on `stream` (staging through `st`).
+static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c,
                          const dg_trace_out* out, bool record, cudaStream_t stream, Stage& st, uint64_t* total_dst) {
   const bool device_mode = c.memory == DG_MEM_DEVICE;
-  const size_t N = size_t(n), L = size_t(lo);
-  auto at = [L](auto* ptr, size_t stride) { return ptr ? ptr + stride * L : ptr; };
+  const size_t N = size_t(n);
+  auto at = [](auto* ptr, size_t) { return ptr; };
   dg::TraceParams p{};
   p.mesh = mesh->view();
   p.n = n;
@@ -480,7 +477,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t lo, int64_t n, const dg_tr
   p.o_transport = st.out(at(out->transport, 9), 9 * N);
   p.o_npoints = st.out(at(out->npoints, 1), N);
   p.o_crossings = st.out(at(out->crossings, 1), N);
-  if (record) {  // never sliced: offsets index the caller's whole polyline arrays
+  if (record) {
     const size_t T = size_t(out->poly_total);
     p.poly_offsets = st.in(out->poly_offsets, N);
     p.poly_face = st.out(out->poly_face, T);
@@ -577,7 +574,7 @@ int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const 
   }
 
   Stage st(stream, device_mode);
-  int rc = enqueue_trace(mesh, 0, n, in, c, out, record, stream, st, out->total_crossings);
+  int rc = enqueue_trace(mesh, n, in, c, out, record, stream, st, out->total_crossings);
   if (rc != DG_OK) return rc;
   cudaError_t e = st.finish();
   if (e != cudaSuccess) return fail_cuda(e, "dg_trace_batch");

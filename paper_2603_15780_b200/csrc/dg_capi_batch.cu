@@ -15,6 +15,8 @@ struct dg_batch {
   int device = 0;  // copy: dg_batch_destroy must not look at the mesh (it may already be gone)
   int64_t cap = 0, n = 0;
   bool traced = false;
+  int32_t traced_max_steps = 0;   // effective step limit of the resident forward traces
+  bool traced_f32 = false;
   static constexpr int kStreams = 8;
   cudaStream_t streams[kStreams] = {};
   // forward inputs and results
@@ -103,6 +105,8 @@ int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace
   if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
   b->traced = false;
   b->n = n;
+  b->traced_max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(b->mesh->nf);
+  b->traced_f32 = c.use_f32 != 0;
   if (n == 0) {
     if (out->total_crossings) *out->total_crossings = 0;
     b->traced = true;
@@ -219,9 +223,15 @@ int dg_batch_gfd(dg_batch* b, double eps_v, double eps_p, const double* g, int32
   dc.stream = st;
   dc.max_steps = max_steps;
   const bool pull = g != nullptr;
-  int rc = dg_gfd_jacobians(b->mesh, n, b->face, b->bary, b->dir, eps_v, eps_p, pull ? b->g : nullptr, &dc, b->jv, b->jp,
-                            b->degraded, nullptr, pull && grad_v ? b->grad_v : nullptr, pull && grad_p ? b->grad_p : nullptr,
-                            nullptr, nullptr, nullptr, err_index);
+  // GFD's base trace of a sample IS its forward trace (diff.cpp:288-294: (p, v), no payload): when the
+  // resident results were traced in f64 under the same step limit they are taken over, bit for bit,
+  // and only the four perturbed traces per sample run
+  const int32_t gfd_steps = max_steps > 0 ? max_steps : default_max_steps(b->mesh->nf);
+  const GfdKnownBase kb{b->o_face, b->o_bary, b->o_dir, b->o_term, b->o_status};
+  const bool reuse = !b->traced_f32 && b->traced_max_steps == gfd_steps && !getenv("DG_BATCH_GFD_RETRACE");
+  int rc = gfd_jacobians_impl(b->mesh, n, b->face, b->bary, b->dir, eps_v, eps_p, pull ? b->g : nullptr, &dc, b->jv, b->jp,
+                              b->degraded, nullptr, pull && grad_v ? b->grad_v : nullptr,
+                              pull && grad_p ? b->grad_p : nullptr, nullptr, nullptr, nullptr, err_index, reuse ? &kb : nullptr);
   if (rc != DG_OK) return rc;
   if (jv) note(cudaMemcpyAsync(jv, b->jv, N * 32, cudaMemcpyDeviceToHost, st));
   if (jp) note(cudaMemcpyAsync(jp, b->jp, N * 32, cudaMemcpyDeviceToHost, st));

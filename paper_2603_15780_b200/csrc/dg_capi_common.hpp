@@ -31,7 +31,6 @@ struct dg_mesh {
   uint8_t* vboundary = nullptr;
   int64_t bytes = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // extra streams of the sliced host-mode pipeline
   // small-batch path: one pinned host block + one device block, reused across calls
   mutable std::mutex small_mu;
   mutable void* small_pin = nullptr;
@@ -144,6 +143,16 @@ class Stage {
   std::vector<void*> allocs_;
   std::vector<Back> backs_;
 };
+
+// Base traces GFD takes over instead of re-tracing them (n entries, same memory space as the other
+// pointers of the call): the forward results of the same samples under the same step limit.
+struct GfdKnownBase {
+  const int32_t* face; const double* bary; const double* dir; const uint8_t* term; const uint8_t* status;
+};
+int gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
+                       double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
+                       uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
+                       double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* known_base);
 
 inline int default_max_steps(int32_t nf) {  // tracer.cpp:543-545
   return int(10.0 * std::sqrt(double(nf))) + 100;

@@ -134,6 +134,28 @@ int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const 
                      double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
                      uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
                      double* base_bary, double* base_dir, int64_t* err_index) {
+  return dgapi::gfd_jacobians_impl(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
+                                   base_face, base_bary, base_dir, err_index, nullptr);
+}
+
+int dg_gfd_jacobians_with_base(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
+                               const int32_t* base_face, const double* base_bary, const double* base_dir,
+                               const uint8_t* base_term, const uint8_t* base_status, double eps_v, double eps_p,
+                               const double* g, const dg_diff_cfg* cfg, double* jv, double* jp, uint8_t* degraded,
+                               double* frames, double* grad_v, double* grad_p, int64_t* err_index) {
+  if (n > 0 && (!base_face || !base_bary || !base_dir || !base_term || !base_status))
+    return fail(DG_ERR_INVALID_ARGS, "dg_gfd_jacobians_with_base: null base trace array");
+  const GfdKnownBase kb{base_face, base_bary, base_dir, base_term, base_status};
+  return dgapi::gfd_jacobians_impl(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
+                                   nullptr, nullptr, nullptr, err_index, &kb);
+}
+
+}  // extern "C"
+
+int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
+                              double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
+                              uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
+                              double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* known_base) {
   if (err_index) *err_index = -1;
   if (int e = check_common(mesh, n, "dg_gfd_jacobians")) return e;
   if (n == 0) return DG_OK;
@@ -177,8 +199,21 @@ int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const 
 
   // round 1: base + perp on the lite kernel, the two payload-carrying seeds on the full kernel
   st.note(dg::launch_gfd_round1_jobs(b, stream));
-  st.note(run_jobs(mesh, 2 * n, b.j1_face, b.j1_bary, b.j1_dir, nullptr, b.r1_face, b.r1_bary, b.r1_dir, nullptr,
-                   b.r1_term, b.r1_status, max_steps, nullptr, stream));
+  if (known_base) {
+    // the base traces are the caller's forward results: only the perp half of the lite jobs runs
+    const cudaMemcpyKind kd = device_mode ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    st.note(cudaMemcpyAsync(b.r1_face, known_base->face, N * sizeof(int32_t), kd, stream));
+    st.note(cudaMemcpyAsync(b.r1_bary, known_base->bary, 3 * N * sizeof(double), kd, stream));
+    st.note(cudaMemcpyAsync(b.r1_dir, known_base->dir, 3 * N * sizeof(double), kd, stream));
+    st.note(cudaMemcpyAsync(b.r1_term, known_base->term, N, kd, stream));
+    st.note(cudaMemcpyAsync(b.r1_status, known_base->status, N, kd, stream));
+    st.note(run_jobs(mesh, n, b.j1_face + N, b.j1_bary + 3 * N, b.j1_dir + 3 * N, nullptr, b.r1_face + N,
+                     b.r1_bary + 3 * N, b.r1_dir + 3 * N, nullptr, b.r1_term + N, b.r1_status + N, max_steps, nullptr,
+                     stream));
+  } else {
+    st.note(run_jobs(mesh, 2 * n, b.j1_face, b.j1_bary, b.j1_dir, nullptr, b.r1_face, b.r1_bary, b.r1_dir, nullptr,
+                     b.r1_term, b.r1_status, max_steps, nullptr, stream));
+  }
   st.note(run_jobs(mesh, 2 * n, b.j1_face + 2 * N, b.j1_bary + 6 * N, b.j1_dir + 6 * N, b.j1_payload + 6 * N,
                    b.r1_face + 2 * N, b.r1_bary + 6 * N, b.r1_dir + 6 * N, b.r1_payload + 6 * N, b.r1_term + 2 * N,
                    b.r1_status + 2 * N, max_steps, nullptr, stream));
@@ -240,5 +275,3 @@ int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const 
   }
   return DG_OK;
 }
-
-}  // extern "C"

@@ -57,6 +57,41 @@ def test_batch_gfd_matches_separate_call(gpu, ref):
     assert np.abs(ours["jv"] - theirs["jv"]).max() <= 1e-5 * scale  # SURVEY.md 8c tolerance
 
 
+def test_batch_gfd_takes_over_the_forward_traces(gpu, ref, monkeypatch):
+    """The resident GFD reuses the forward results as its base traces: same bits as a re-trace,
+    same whole-call failure when a base trace leaves the mesh (diff.cpp:121-124)."""
+    rm = ref.RefMesh.icosphere(4)
+    m = gpu_mesh(gpu, rm)
+    n = 2500
+    f, b, d = rm.sample_queries(5, n, 0.1, 1.0)
+    g = unit_rows(np.random.default_rng(4), n)
+    batch = gpu.Batch(m, n)
+    batch.trace(f, b, d)
+    reused = batch.gfd(g=g)
+    monkeypatch.setenv("DG_BATCH_GFD_RETRACE", "1")
+    retraced = batch.gfd(g=g)
+    monkeypatch.delenv("DG_BATCH_GFD_RETRACE")
+    for k in ("jv", "jp", "degraded", "grad_v", "grad_p"):
+        assert np.array_equal(reused[k], retraced[k]), k
+    h = m.trace_batch(f, b, d)
+    given = m.gfd(f, b, d, g=g, base=h)  # dg_gfd_jacobians_with_base: gfd_batched's `trace` argument
+    for k in ("jv", "jp", "degraded", "grad_v", "grad_p", "frames"):
+        assert np.array_equal(given[k], m.gfd(f, b, d, g=g)[k]), k
+    batch.trace(f, b, d, max_steps=7)  # a different step limit: the forward traces are not GFD's base traces
+    limited = batch.gfd(g=g)
+    assert np.array_equal(limited["jv"], reused["jv"])
+    pl = ref.RefMesh.plane(6, 6, 1.0, 0)
+    mp = gpu_mesh(gpu, pl)
+    fp, bp, dp = pl.sample_queries(2, 64, 0.01, 0.05)
+    dp[17] *= 1e3  # leaves through the boundary
+    bt = gpu.Batch(mp, 64)
+    h = bt.trace(fp, bp, dp)
+    assert h.term[17] == 1
+    with pytest.raises(gpu.DgError) as e:
+        bt.gfd()
+    assert "base trace did not reach" in e.value.msg and e.value.index == 17
+
+
 def test_batch_contract_errors(gpu, ref):
     rm = ref.RefMesh.icosphere(2)
     m = gpu_mesh(gpu, rm)
