@@ -98,3 +98,30 @@ def test_rejected_and_degenerate_starts(gpu):
     d[70] = [np.nan, 0.0, 1.0]
     r = both_walkers(m, f, b, d)
     assert list(r.stall[[10, 11, 20, 40]]) == [4, 4, 5, 3] and r.traced[30] == 0.0
+
+
+@pytest.mark.parametrize("key,n", [("c2", 60_000), ("c3", 12_000)])
+def test_baseline_configs_against_the_reference(gpu, ref, key, n):
+    """BASELINE.json's meshes at full size (config 2: 81 920 faces with crossing records; config 3:
+    1 M faces, face records only) on a prefix of the benchmark's own query stream: final face,
+    barycentrics, direction, traced length and the whole face sequence against the UNMODIFIED
+    reference -- bit for bit (random starts never take a vertex branch), plus EP gradients."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import make_workload
+    xyz, tri, f, b, d, q = make_workload(key, n, 42)
+    m = gpu.Mesh(xyz, tri)
+    assert m.has_transport_cache == (key == "c2")
+    rm = ref.RefMesh.build(xyz, tri)
+    ours = both_walkers(m, f, b, d)
+    theirs = rm.trace_batch(f, b, d, record_polyline=True)
+    for k in ("face", "bary", "dir", "traced", "requested", "term", "status"):
+        assert np.array_equal(getattr(ours, k), getattr(theirs, k)), k
+    assert np.array_equal(ours.npoints, theirs.npoints)
+    assert ours.total_crossings == int((theirs.npoints - 2).sum())  # one polyline point per advance + the start
+    poly = m.trace_batch(f[:2000], b[:2000], d[:2000], record_polyline=True)
+    keep = theirs.poly_offsets[2000]
+    assert np.array_equal(poly.poly_face, theirs.poly_face[:keep]) and np.array_equal(poly.poly_bary, theirs.poly_bary[:keep])
+    g = 2.0 * (m.embed(ours.face, ours.bary) - q)  # gradcheck.cpp:88
+    assert np.array_equal(m.ep_backward(f, d, ours.face, ours.dir, g),
+                          rm.ep(f, b, d, theirs.face, theirs.bary, theirs.dir, g=g)["grad_v"])
