@@ -108,7 +108,7 @@ DG_API int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int
 /* Same, with layout flags. The transport cache stores one 128-byte crossing record per directed
  * half-edge: the fold isometry of tracer.cpp:113-126 plus the two corner-0 edge vectors of the
  * entered face (computed on the device at upload by the same code the uncached walker runs, so
- * results are bit-identical). AUTO enables it while the records stay within 200 MB (about 520 k
+ * results are bit-identical). AUTO enables it while the records stay within 250 MB (about 650 k
  * faces) -- beyond that they outgrow the TLB reach and the uncached walker is faster; env
  * DG_TRANSPORT_CACHE=on|off overrides AUTO. */
 enum { DG_MESH_TRANSPORT_AUTO = 0, DG_MESH_TRANSPORT_ON = 1, DG_MESH_TRANSPORT_OFF = 2 };

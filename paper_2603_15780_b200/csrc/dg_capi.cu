@@ -311,7 +311,7 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
       // beyond the L2) and drops to 19.7 Gcross/s at 1 M faces (384 MB), where the uncached walker
       // (96 B per face) holds 26-29 Gcross/s: the cliff sits where the records outgrow the 256 MB
       // reach of the TLB (2 MB pages), not where they outgrow the L2.
-      cache = 3 * F * sizeof(dg::HalfEdgeRec) <= (size_t(200) << 20);
+      cache = 3 * F * sizeof(dg::HalfEdgeRec) <= (size_t(250) << 20);
     }
   }
   if (cache) {
