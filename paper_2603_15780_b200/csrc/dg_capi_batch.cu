@@ -23,7 +23,8 @@ struct dg_batch {
   int32_t *face = nullptr, *o_face = nullptr, *o_npoints = nullptr, *o_crossings = nullptr;
   double *bary = nullptr, *dir = nullptr, *o_bary = nullptr, *o_dir = nullptr, *o_traced = nullptr, *o_requested = nullptr;
   uint8_t *o_term = nullptr, *o_status = nullptr, *o_stall = nullptr;
-  uint64_t* totals = nullptr;  // [kStreams] per-slice crossing counts
+  uint64_t* totals = nullptr;  // [kStreams] per-slice crossing counts / EP error words (device)
+  uint64_t* words = nullptr;   // [kStreams] pinned host mirror (a pageable target would make the copy block)
   // backward
   double *g = nullptr, *grad_v = nullptr, *grad_p = nullptr, *jv = nullptr, *jp = nullptr;
   uint8_t* degraded = nullptr;
@@ -66,6 +67,7 @@ int dg_batch_create(const dg_mesh* mesh, int64_t capacity, dg_batch** out) {
   ok(dev_alloc(&b->o_term, N)); ok(dev_alloc(&b->o_status, N)); ok(dev_alloc(&b->o_stall, N));
   ok(dev_alloc(&b->o_npoints, N)); ok(dev_alloc(&b->o_crossings, N));
   ok(dev_alloc(&b->totals, size_t(dg_batch::kStreams)));
+  ok(cudaMallocHost(reinterpret_cast<void**>(&b->words), dg_batch::kStreams * sizeof(uint64_t)));
   ok(dev_alloc(&b->g, 3 * N)); ok(dev_alloc(&b->grad_v, 3 * N)); ok(dev_alloc(&b->grad_p, 3 * N));
   if (e != cudaSuccess) {
     dg_batch_destroy(b);
@@ -82,6 +84,7 @@ void dg_batch_destroy(dg_batch* b) {
   cudaFree(b->face); cudaFree(b->bary); cudaFree(b->dir); cudaFree(b->o_face); cudaFree(b->o_bary); cudaFree(b->o_dir);
   cudaFree(b->o_traced); cudaFree(b->o_requested); cudaFree(b->o_term); cudaFree(b->o_status); cudaFree(b->o_stall);
   cudaFree(b->o_npoints); cudaFree(b->o_crossings); cudaFree(b->totals);
+  if (b->words) cudaFreeHost(b->words);
   cudaFree(b->g); cudaFree(b->grad_v); cudaFree(b->grad_p); cudaFree(b->jv); cudaFree(b->jp); cudaFree(b->degraded);
   delete b;
 }
@@ -176,29 +179,30 @@ int dg_batch_ep_backward(dg_batch* b, const double* g, double* grad_v, double* g
   const int S = slices_for(n);
   cudaError_t e = cudaSuccess;
   auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
-  for (int s = 0; s < S; ++s) {  // all uploads are in flight before the first kernel is waited for
+  // per slice: g in, fused kernel, gradients out -- nothing waits on the host until every slice is queued
+  // (totals[] doubles as the per-slice error words)
+  uint64_t* words = b->words;
+  for (int s = 0; s < S; ++s) {
     const size_t L = size_t(n * s / S), M = size_t(n * (s + 1) / S) - L;
-    note(cudaMemcpyAsync(b->g + 3 * L, g + 3 * L, M * 24, cudaMemcpyHostToDevice, b->streams[s]));
-  }
-  int rc = DG_OK;
-  for (int s = 0; s < S && rc == DG_OK; ++s) {
-    const size_t L = size_t(n * s / S), M = size_t(n * (s + 1) / S) - L;
-    dg_diff_cfg dc{};
-    dc.memory = DG_MEM_DEVICE;
-    dc.stream = b->streams[s];
-    int64_t idx = -1;
-    rc = dg_ep_backward(b->mesh, int64_t(M), b->face + L, b->dir + 3 * L, b->o_face + L, b->o_dir + 3 * L, b->g + 3 * L,
-                        &dc, b->grad_v + 3 * L, grad_p ? b->grad_p + 3 * L : nullptr, &idx);
-    if (rc != DG_OK) {
-      if (err_index && idx >= 0) *err_index = idx + int64_t(L);
-      break;
-    }
-    note(cudaMemcpyAsync(grad_v + 3 * L, b->grad_v + 3 * L, M * 24, cudaMemcpyDeviceToHost, b->streams[s]));
-    if (grad_p) note(cudaMemcpyAsync(grad_p + 3 * L, b->grad_p + 3 * L, M * 24, cudaMemcpyDeviceToHost, b->streams[s]));
+    cudaStream_t st = b->streams[s];
+    unsigned long long* word = reinterpret_cast<unsigned long long*>(b->totals + s);
+    note(cudaMemcpyAsync(b->g + 3 * L, g + 3 * L, M * 24, cudaMemcpyHostToDevice, st));
+    note(ep_backward_enqueue(b->mesh, int64_t(M), b->face + L, b->dir + 3 * L, b->o_face + L, b->o_dir + 3 * L,
+                             b->g + 3 * L, b->grad_v + 3 * L, grad_p ? b->grad_p + 3 * L : nullptr, word, st));
+    note(cudaMemcpyAsync(grad_v + 3 * L, b->grad_v + 3 * L, M * 24, cudaMemcpyDeviceToHost, st));
+    if (grad_p) note(cudaMemcpyAsync(grad_p + 3 * L, b->grad_p + 3 * L, M * 24, cudaMemcpyDeviceToHost, st));
+    note(cudaMemcpyAsync(&words[s], word, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   }
   for (int s = 0; s < S; ++s) note(cudaStreamSynchronize(b->streams[s]));
-  if (rc != DG_OK) return rc;
   if (e != cudaSuccess) return fail_cuda(e, "dg_batch_ep_backward");
+  for (int s = 0; s < S; ++s) {  // the first failing sample in request order
+    int64_t idx = -1;
+    const int rc = ep_error_to_rc(words[s], "dg_batch_ep_backward", &idx);
+    if (rc != DG_OK) {
+      if (err_index) *err_index = idx + n * s / S;
+      return rc;
+    }
+  }
   return DG_OK;
 }
 

@@ -154,6 +154,14 @@ int gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* face, cons
                        uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
                        double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* known_base);
 
+// EP backward on device-resident arrays without a host round trip: *err_word (device) receives
+// kEpNoError or (sample index << 2 | reason), decoded by ep_error_to_rc after the stream is synced.
+constexpr unsigned long long kEpNoError = ~0ull;
+cudaError_t ep_backward_enqueue(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* v,
+                                const int32_t* end_face, const double* end_dir, const double* g, double* grad_v,
+                                double* grad_p, unsigned long long* err_word, cudaStream_t stream);
+int ep_error_to_rc(unsigned long long word, const char* who, int64_t* err_index);
+
 inline int default_max_steps(int32_t nf) {  // tracer.cpp:543-545
   return int(10.0 * std::sqrt(double(nf))) + 100;
 }

@@ -102,16 +102,7 @@ static int ep_common(const dg_mesh* mesh, int64_t n, const int32_t* face, const 
   st.note(cudaStreamSynchronize(stream));  // the return code depends on the error word
   cudaError_t e = st.finish();
   if (e != cudaSuccess) return fail_cuda(e, who);
-  if (h_err != kNoError) {
-    const int64_t idx = int64_t(h_err >> 2);
-    if (err_index) *err_index = idx;
-    switch (int(h_err & 3ull)) {
-      case 0: return fail(DG_ERR_DEGENERATE_DIRECTION, "ep_jacobians: |v| too small");
-      case 1: return fail(DG_ERR_DEGENERATE_DIRECTION, "direction is normal to the face");
-      default: return fail(DG_ERR_INVALID_ARGS, "%s: face index out of range at sample %lld", who, (long long)idx);
-    }
-  }
-  return DG_OK;
+  return dgapi::ep_error_to_rc(h_err, who, err_index);
 }
 
 int dg_ep_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
@@ -151,6 +142,31 @@ int dg_gfd_jacobians_with_base(const dg_mesh* mesh, int64_t n, const int32_t* fa
 }
 
 }  // extern "C"
+
+cudaError_t dgapi::ep_backward_enqueue(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* v,
+                                       const int32_t* end_face, const double* end_dir, const double* g, double* grad_v,
+                                       double* grad_p, unsigned long long* err_word, cudaStream_t stream) {
+  dg::EpParams p{};
+  p.mesh = mesh->view();
+  p.n = n;
+  p.face = face; p.v = v; p.end_face = end_face; p.end_dir = end_dir; p.g = g;
+  p.grad_v = grad_v; p.grad_p = grad_p;
+  p.first_error = err_word;
+  cudaError_t e = cudaMemsetAsync(err_word, 0xff, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  return dg::launch_ep(p, stream);
+}
+
+int dgapi::ep_error_to_rc(unsigned long long word, const char* who, int64_t* err_index) {
+  if (word == kEpNoError) return DG_OK;
+  const int64_t idx = int64_t(word >> 2);
+  if (err_index) *err_index = idx;
+  switch (int(word & 3ull)) {
+    case 0: return fail(DG_ERR_DEGENERATE_DIRECTION, "ep_jacobians: |v| too small");
+    case 1: return fail(DG_ERR_DEGENERATE_DIRECTION, "direction is normal to the face");
+    default: return fail(DG_ERR_INVALID_ARGS, "%s: face index out of range at sample %lld", who, (long long)idx);
+  }
+}
 
 int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
                               double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
