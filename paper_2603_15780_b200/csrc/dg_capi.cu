@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "dg_capi_common.hpp"
+#include "dg_fast_walk.cuh"
 #include "dg_tracer_core.cuh"
 
 namespace dgapi {
@@ -63,25 +64,7 @@ __global__ void build_halfedges_kernel(const dg::MeshView m, dg::HalfEdgeRec* he
   const int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (s >= 3 * int64_t(m.nf)) return;
   const int f = int(s / 3), k = int(s % 3);
-  const Face<double> c = load_face<double>(m, f);
-  HalfEdgeRec r{};
-  r.g = c.adj(k);
-  if (r.g >= 0) {
-    const int ka = (k + 1) % 3, kc = (k + 2) % 3;
-    const int va = c.id(ka), vc = c.id(kc);
-    const Face<double> G = load_face<double>(m, r.g);
-    const int vt = G.third(va, vc);
-    const EdgeTransport<double> t =
-        Tracer<double, false>::make_edge_transport(c.pos(ka), c.pos(kc), c.pos(k), G.pos_of(vt));
-    r.t[0] = t.edge.x; r.t[1] = t.edge.y; r.t[2] = t.edge.z;
-    r.t[3] = t.in_from.x; r.t[4] = t.in_from.y; r.t[5] = t.in_from.z;
-    r.t[6] = t.in_to.x; r.t[7] = t.in_to.y; r.t[8] = t.in_to.z;
-    r.corners = G.corner_of(va) | (G.corner_of(vc) << 2) | (G.corner_of(vt) << 4);
-    // the face-only operands of wedge_coeffs(g, 0, .), tracer.cpp:130-133
-    const V3<double> e1 = G.x1 - G.x0, e2 = G.x2 - G.x0;
-    r.e[0] = e1.x; r.e[1] = e1.y; r.e[2] = e1.z;
-    r.e[3] = e2.x; r.e[4] = e2.y; r.e[5] = e2.z;
-  }
+  const HalfEdgeRec r = make_halfedge_rec(m, f, k);
   he[s] = r;
 }
 

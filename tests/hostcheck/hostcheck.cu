@@ -8,6 +8,8 @@
 #include <cstdint>
 #include <vector>
 
+#define DG_HOSTCHECK 1
+#include "../../paper_2603_15780_b200/csrc/dg_fast_walk.cuh"
 #include "../../paper_2603_15780_b200/csrc/dg_tracer_core.cuh"
 
 using namespace dg;
@@ -18,15 +20,47 @@ namespace {
 
 struct HostMesh {
   std::vector<FaceRec> rec;
+  std::vector<HalfEdgeRec> he;  // crossing records (built on demand by the same function the upload kernel runs)
   std::vector<double> fnormal, vangle;
   std::vector<int32_t> csr_off, csr_list;
   std::vector<uint8_t> vboundary;
   int32_t nf, nv;
-  MeshView view() const {
-    return MeshView{rec.data(), nullptr, fnormal.data(), vangle.data(), csr_off.data(), csr_list.data(),
-                    vboundary.data(), nf, nv};
+  MeshView view(bool cached = false) const {
+    return MeshView{rec.data(), cached ? he.data() : nullptr, fnormal.data(), vangle.data(), csr_off.data(),
+                    csr_list.data(), vboundary.data(), nf, nv};
   }
 };
+
+// The fast walker (csrc/dg_fast_walk.cuh) driven the way trace_fast_kernel drives a lane: lean
+// start-up, fast steps, the generic paths for everything the fast step hands back.
+template <bool kCached>
+void run_fast(const HostMesh& hm, const TraceParams& p) {
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int64_t q = 0; q < p.n; ++q) {
+    FastLane<kCached> L{};
+    const V3<double> qb{p.bary[3 * q], p.bary[3 * q + 1], p.bary[3 * q + 2]};
+    const V3<double> qv{p.dir[3 * q], p.dir[3 * q + 1], p.dir[3 * q + 2]};
+    bool live = fast_init<kCached>(p.mesh, p.face[q], qb, qv, L);
+    if (!live) {
+      LaneState S;
+      live = lane_init<kCached>(p, q, &S);
+      lane_in<kCached>(p.mesh, S, L);
+    }
+    while (live) {
+      StepSpill sp;
+      const int action = fast_step<kCached>(p.mesh, p.max_steps, L, sp);
+      if (action == kActFast) continue;
+      if (action == kActFinish) {
+        fast_finish<kCached>(p, q, L, sp);
+        break;
+      }
+      LaneState S;
+      lane_out<kCached>(L, sp, S);
+      live = lane_generic<kCached>(p, q, &S, action);
+      lane_in<kCached>(p.mesh, S, L);
+    }
+  }
+}
 
 template <class S>
 void run_batch(const HostMesh& hm, int64_t n, const int32_t* face, const double* bary, const double* dir,
@@ -106,4 +140,27 @@ HC_API void hc_trace_batch(void* h, int64_t n, const int32_t* face, const double
   else
     run_batch<double>(hm, n, face, bary, dir, payload, max_steps, hole, want_q, o_face, o_bary, o_dir, o_traced,
                       o_requested, o_term, o_status, o_stall, o_payload, o_q, o_npoints, o_crossings, poly_off, pf, pb, ps);
+}
+
+// The fast walker on the host, with (cached = 1) or without crossing records. fast_steps (may be
+// null) receives how many transitions the fast step committed, to prove it is the path under test.
+HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const double* bary, const double* dir,
+                                int max_steps, int cached, int32_t* o_face, double* o_bary, double* o_dir,
+                                double* o_traced, double* o_requested, uint8_t* o_term, uint8_t* o_status,
+                                uint8_t* o_stall, int32_t* o_npoints, int32_t* o_crossings) {
+  HostMesh& hm = *static_cast<HostMesh*>(h);
+  if (cached && hm.he.empty()) {
+    hm.he.resize(3 * size_t(hm.nf));
+    const MeshView mv = hm.view(false);
+    for (int f = 0; f < hm.nf; ++f)
+      for (int k = 0; k < 3; ++k) hm.he[3 * size_t(f) + k] = make_halfedge_rec(mv, f, k);
+  }
+  TraceParams p{};
+  p.mesh = hm.view(cached != 0);
+  p.n = n;
+  p.face = face; p.bary = bary; p.dir = dir;
+  p.o_face = o_face; p.o_bary = o_bary; p.o_dir = o_dir; p.o_traced = o_traced; p.o_requested = o_requested;
+  p.o_term = o_term; p.o_status = o_status; p.o_stall = o_stall; p.o_npoints = o_npoints; p.o_crossings = o_crossings;
+  p.max_steps = max_steps;
+  if (cached) run_fast<true>(hm, p); else run_fast<false>(hm, p);
 }

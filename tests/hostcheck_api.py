@@ -17,7 +17,8 @@ CORE = os.path.join(HERE, "..", "paper_2603_15780_b200", "csrc")
 
 
 def build(force=False):
-    deps = [SRC] + [os.path.join(CORE, f) for f in ("dg_tracer_core.cuh", "dg_mesh_view.cuh", "dg_math.cuh")]
+    deps = [SRC] + [os.path.join(CORE, f) for f in ("dg_tracer_core.cuh", "dg_mesh_view.cuh", "dg_math.cuh",
+                                                     "dg_fast_walk.cuh", "dg_kernels.cuh")]
     if not force and os.path.exists(SO) and all(os.path.getmtime(SO) >= os.path.getmtime(d) for d in deps):
         return SO
     os.makedirs(os.path.dirname(SO), exist_ok=True)
@@ -84,4 +85,21 @@ class HostMesh:
             call(off, r.poly_face, r.poly_bary, r.poly_seg)
         if payload is not None:
             r.has_payload = (np.square(payload).sum(1) > 0).astype(np.uint8)
+        return r
+
+    def trace_batch_fast(self, face, bary, dirs, max_steps=0, cached=False):
+        """The fast walker (csrc/dg_fast_walk.cuh: fast_init / fast_step / fast_finish + the generic
+        paths behind them) driven on the host the way trace_fast_kernel drives a lane."""
+        face, bary, dirs = _i32(face), _f64(bary), _f64(dirs)
+        n = len(face)
+        if max_steps <= 0:
+            max_steps = int(10.0 * np.sqrt(float(self.nf))) + 100
+        r = TraceResult(face=np.empty(n, np.int32), bary=np.empty((n, 3)), dir=np.empty((n, 3)),
+                        traced=np.empty(n), requested=np.empty(n), term=np.empty(n, np.uint8),
+                        status=np.empty(n, np.uint8), npoints=np.empty(n, np.int32))
+        r.stall = np.empty(n, np.uint8)
+        r.crossings = np.empty(n, np.int32)
+        lib().hc_trace_batch_fast(self.h, C.c_int64(n), _p(face), _p(bary), _p(dirs), int(max_steps), int(cached),
+                                  _p(r.face), _p(r.bary), _p(r.dir), _p(r.traced), _p(r.requested), _p(r.term),
+                                  _p(r.status), _p(r.stall), _p(r.npoints), _p(r.crossings))
         return r

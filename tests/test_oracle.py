@@ -77,6 +77,54 @@ def test_device_state_machine_on_host_matches_fixtures(hostcheck, oracle, path):
     check_against_fixture(z, r, exact=True)
 
 
+@pytest.mark.parametrize("cached", [False, True], ids=["face-records", "crossing-records"])
+@pytest.mark.parametrize("path", TRACE_FIXTURES, ids=[os.path.basename(p)[:-4] for p in TRACE_FIXTURES])
+def test_fast_walker_on_host_matches_fixtures(hostcheck, oracle, path, cached):
+    """The fast walker (csrc/dg_fast_walk.cuh: lean start-up, fast step, finish, and the generic
+    paths it hands everything else to) compiled for the host and driven the way the kernel drives
+    a lane: end states and counters of the reference fixtures, bit for bit, on both mesh layouts.
+    (A payload or a transport matrix rides along without changing the path, so those fixtures pin
+    the fast walker's end states too; hole avoidance changes the path and belongs to the general
+    walker only.)"""
+    z = np.load(path)
+    if z["cfg"][1]:
+        pytest.skip("hole avoidance: general walker")
+    a = oracle.OracleMesh(z["xyz"], z["tri"]).arrays()
+    hm = hostcheck.HostMesh(a)
+    r = hm.trace_batch_fast(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), cached=cached)
+    for k in ("face", "term", "status", "npoints"):
+        assert np.array_equal(z["o_" + k], getattr(r, k)), k
+    for k, got in (("o_bary", r.bary), ("o_dir", r.dir), ("o_traced", r.traced), ("o_requested", r.requested)):
+        assert _equal(z[k], got), f"{k} not bit-equal"
+    g = hm.trace_batch(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]))
+    assert np.array_equal(g.crossings, r.crossings) and np.array_equal(g.stall, r.stall)
+
+
+@pytest.mark.parametrize("cached", [False, True], ids=["face-records", "crossing-records"])
+def test_fast_walker_on_host_vs_reference_fresh_inputs(hostcheck, ref, cached):
+    """Differential check of the host-compiled fast walker against the unmodified reference on
+    meshes and inputs that are not in the fixtures, including every way out of the fast step:
+    vertex starts, edge starts, axis-aligned directions on a flat grid (exact zeros), boundary
+    stops, a tight step limit, rejected and zero-length starts."""
+    cases = [(ref.RefMesh.icosphere(4), 81, 0.1, 3.0, 0), (ref.RefMesh.torus(1 / 3, 1 / 6, 48, 24), 82, 0.05, 2.0, 0),
+             (ref.RefMesh.plane(10, 8, 1.0, 0), 83, 0.05, 2.0, 0), (ref.RefMesh.cylinder(0.5, 1.0, 16, 4), 84, 0.05, 3.0, 0),
+             (ref.RefMesh.icosphere(3), 85, 1.0, 6.0, 9)]
+    for rm, seed, lo, hi, max_steps in cases:
+        hm = hostcheck.HostMesh(rm.arrays())
+        f, b, d = rm.sample_queries(seed, 4000, lo, hi)
+        d[:400] = np.array([1.0, 0.0, 0.0]) * np.linalg.norm(d[:400], axis=1, keepdims=True)   # may leave the face plane: projected
+        b[400:500] = [0.5, 0.5, 0.0]
+        b[500:600] = [0.0, 1.0, 0.0]
+        f[600] = -1; b[601] = [0.9, 0.9, 0.9]; d[602] = 0.0
+        theirs = rm.trace_batch(f, b, d, record_polyline=True, max_steps=max_steps)
+        ours = hm.trace_batch_fast(f, b, d, max_steps=max_steps or rm.default_max_steps(), cached=cached)
+        for k in ("face", "term", "status", "npoints"):
+            assert np.array_equal(getattr(theirs, k), getattr(ours, k)), k
+        for k in ("bary", "dir", "traced", "requested"):
+            assert _equal(getattr(theirs, k), getattr(ours, k)), k   # same libm on the host: exact on vertex branches too
+        assert (ours.crossings[ours.term == 0] >= 0).all()
+
+
 def test_golden_square_trace_values(oracle):
     """proj/tests/golden/trace_square.json, compared bit-for-bit by the reference (test_io.cpp:71-82)."""
     m = oracle.OracleMesh([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]], [[0, 1, 2], [0, 2, 3]])
