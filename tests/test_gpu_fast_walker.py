@@ -125,3 +125,14 @@ def test_baseline_configs_against_the_reference(gpu, ref, key, n):
     g = 2.0 * (m.embed(ours.face, ours.bary) - q)  # gradcheck.cpp:88
     assert np.array_equal(m.ep_backward(f, d, ours.face, ours.dir, g),
                           rm.ep(f, b, d, theirs.face, theirs.bary, theirs.dir, g=g)["grad_v"])
+
+
+def test_randomised_meshes_scales_and_starts(gpu):
+    """scripts/fuzz_walkers.py, a short run: random mesh families at scales from 1e-160 to 1e+160
+    (the operand-range guards of the hand-expanded divisions), slivers, lengths over 9 decades,
+    vertex / edge / along-edge / rejected starts, tight step limits -- fast walker == general walker
+    bit for bit on both layouts, and the two layouts agree."""
+    import os, sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    import fuzz_walkers
+    assert fuzz_walkers.main(rounds=24, n=6000, seed=11) == 0
