@@ -257,7 +257,8 @@ DG_API int dg_gfd_jacobians_with_base(const dg_mesh* mesh, int64_t n, const int3
  * samples. A dg_batch keeps the forward inputs and results of that step on the GPU between the
  * two calls, so the backward moves only the upstream gradient in and the gradients out. All
  * pointers are HOST pointers (pinned memory lets the copies overlap the kernels); the arithmetic
- * is that of dg_trace_batch / dg_ep_backward / dg_gfd_jacobians, bit for bit. */
+ * is that of dg_trace_batch / dg_ep_backward / dg_gfd_jacobians, bit for bit. A dg_batch is not
+ * thread-safe (one per calling thread); it must be destroyed before its mesh. */
 typedef struct dg_batch dg_batch;
 DG_API int dg_batch_create(const dg_mesh* mesh, int64_t capacity, dg_batch** out);
 DG_API void dg_batch_destroy(dg_batch* b);
