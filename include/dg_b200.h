@@ -133,7 +133,8 @@ typedef struct dg_trace_cfg {
   uint8_t memory;                /* DG_MEM_HOST: pointers are host memory, staged by the library
                                     DG_MEM_DEVICE: pointers are device memory on the mesh's GPU */
   uint8_t sort_by_face;          /* schedule queries in start-face order (results stay at request index) */
-  uint8_t refill_min;            /* idle lanes a warp waits for before it steals work (0 = default 1) */
+  uint8_t refill_min;            /* idle lanes a warp waits for before it steals work (0 = the walker's default:
+                                    4 with a bounded wait for the fast walker, 1 for the general one) */
   uint8_t blocks_per_sm;         /* resident CTAs per SM of the persistent grid (0 = occupancy query) */
   uint8_t walker;                /* DG_WALKER_AUTO: the fast walker whenever the request is the plain f64
                                     forward map; DG_WALKER_GENERIC: always the general state machine

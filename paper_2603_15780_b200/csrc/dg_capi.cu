@@ -423,7 +423,7 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   p.queue_head = reinterpret_cast<unsigned long long*>(dp);
   p.total_crossings = reinterpret_cast<unsigned long long*>(dout(12));
   p.max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
-  p.refill_min = 1;
+  p.refill_min = 0;
   p.hole_avoidance = c.hole_avoidance;
   p.want_q = c.want_transport_matrix;
   if (p.total_crossings) DG_CUDA(cudaMemsetAsync(p.total_crossings, 0, 8, stream));
@@ -468,7 +468,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
     p.poly_seg = st.out(out->poly_seg, T);
   }
   p.max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
-  p.refill_min = c.refill_min ? c.refill_min : 1;
+  p.refill_min = c.refill_min;  // 0 = the walker's own default
   p.hole_avoidance = c.hole_avoidance;
   p.want_q = c.want_transport_matrix;
 

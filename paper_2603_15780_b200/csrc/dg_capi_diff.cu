@@ -24,7 +24,7 @@ cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const do
   p.face = jf; p.bary = jb; p.dir = jd; p.payload = jp;
   p.o_face = rf; p.o_bary = rb; p.o_dir = rd; p.o_payload = rp; p.o_term = rt; p.o_status = rs;
   p.max_steps = max_steps;
-  p.refill_min = 1;
+  p.refill_min = 0;  // the walker's own default
   unsigned long long* ctr = mesh->next_counters();
   p.queue_head = ctr;
   p.total_crossings = total;

@@ -38,7 +38,7 @@ struct TraceParams {
   unsigned long long* queue_head;       // work-stealing cursor, zeroed before the launch
   unsigned long long* total_crossings;  // optional: += sum of crossings of the batch
   int32_t max_steps;
-  int32_t refill_min;  // refill a warp once this many lanes are idle (>= 1)
+  int32_t refill_min;  // refill a warp once this many lanes are idle (0 = the walker's default)
   uint8_t hole_avoidance;
   uint8_t want_q;
 };
