@@ -72,7 +72,7 @@ enum { DG_EVENT_ADVANCED = 0, DG_EVENT_CROSSED_EDGE = 1, DG_EVENT_CROSSED_VERTEX
        DG_EVENT_BOUNDARY_SLIDE = 3, DG_EVENT_BOUNDARY_STOP = 4 };
 
 enum { DG_MEM_HOST = 0, DG_MEM_DEVICE = 1 };
-enum { DG_WALKER_AUTO = 0, DG_WALKER_GENERIC = 1 };
+enum { DG_WALKER_AUTO = 0, DG_WALKER_GENERIC = 1, DG_WALKER_FAST_LOADS = 2, DG_WALKER_FAST_TMA = 3 };
 /* Arithmetic of the f64 tracer: there is ONE lane. The library is built without FMA contraction
  * and follows the reference's operation order, so a trace that never takes a vertex branch (no
  * libm calls) is bit-identical to the reference CPU build; vertex branches agree to the last
@@ -137,8 +137,11 @@ typedef struct dg_trace_cfg {
                                     4 with a bounded wait for the fast walker, 1 for the general one) */
   uint8_t blocks_per_sm;         /* resident CTAs per SM of the persistent grid (0 = occupancy query) */
   uint8_t walker;                /* DG_WALKER_AUTO: the fast walker whenever the request is the plain f64
-                                    forward map; DG_WALKER_GENERIC: always the general state machine
-                                    (same bits; kept selectable for cross-checks and measurements) */
+                                    forward map, gathering the crossing records with 256-bit loads up to
+                                    250 MB of records and through TMA tile::gather4 beyond;
+                                    DG_WALKER_GENERIC: always the general state machine; DG_WALKER_FAST_LOADS /
+                                    DG_WALKER_FAST_TMA: the fast walker with that gather. Same bits whatever
+                                    the choice; selectable for cross-checks and measurements */
   uint8_t reserved[3];
   void* stream;                  /* cudaStream_t to launch on. DG_MEM_HOST: NULL = the mesh's private
                                     stream, the call returns when the results are in host memory.

@@ -132,7 +132,7 @@ class Mesh:
     # ------------------------------------------------------------------ forward tracing
     def trace_batch(self, face, bary, dirs, payload=None, max_steps=0, hole_avoidance=False, want_q=False,
                     record_polyline=False, use_f32=False, sort_by_face=False, refill_min=0, blocks_per_sm=0,
-                    out=None, generic_walker=False):
+                    out=None, generic_walker=False, walker="auto"):
         """trace_batch (tracer.cpp:596) on host arrays; results at the request index. `out`: a
         TraceResult of a previous call of the same size whose (e.g. pinned) arrays are reused."""
         h = self._handle()
@@ -155,7 +155,7 @@ class Mesh:
         cfg = TraceCfg(max_steps=int(max_steps), hole_avoidance=int(hole_avoidance),
                        want_transport_matrix=int(want_q), use_f32=int(use_f32), memory=capi.MEM_HOST,
                        sort_by_face=int(sort_by_face), refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm),
-                       walker=int(generic_walker))
+                       walker=1 if generic_walker else WALKERS[walker])
         tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), ptr(payload))
         total = C.c_uint64(0)
 
@@ -183,7 +183,7 @@ class Mesh:
 
     def trace_batch_device(self, face, bary, dirs, out, payload=None, max_steps=0, hole_avoidance=False,
                            want_q=False, stream=None, sort_by_face=False, refill_min=0, blocks_per_sm=0,
-                           generic_walker=False):
+                           generic_walker=False, walker="auto"):
         """Zero-copy entry point: every array is a torch CUDA tensor on the mesh's device;
         `out` maps dg_trace_out field names to preallocated tensors. Asynchronous on `stream`."""
         import torch
@@ -191,7 +191,8 @@ class Mesh:
         n = int(face.numel())
         cfg = TraceCfg(max_steps=int(max_steps), hole_avoidance=int(hole_avoidance),
                        want_transport_matrix=int(want_q), memory=capi.MEM_DEVICE, sort_by_face=int(sort_by_face),
-                       refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm), walker=int(generic_walker),
+                       refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm),
+                       walker=1 if generic_walker else WALKERS[walker],
                        stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
         tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), ptr(payload))
         o = TraceOut()
@@ -306,6 +307,10 @@ class Mesh:
         check(lib().dg_gfd_jacobians(self._handle(), int(face.numel()), ptr(face), ptr(bary), ptr(v), float(eps_v),
                                      float(eps_p), ptr(g), C.addressof(cfg), ptr(jv), ptr(jp), ptr(degraded), None,
                                      ptr(grad_v), ptr(grad_p), None, None, None, C.addressof(ei)), ei)
+
+
+# dg_trace_cfg.walker (DG_WALKER_*): which kernel traces a plain f64 forward request
+WALKERS = {"auto": 0, "generic": 1, "loads": 2, "tma": 3}
 
 
 class Batch:

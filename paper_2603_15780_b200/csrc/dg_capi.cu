@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda.h>
+
 #include "dg_capi_common.hpp"
 #include "dg_fast_walk.cuh"
 #include "dg_tracer_core.cuh"
@@ -66,6 +68,32 @@ __global__ void build_halfedges_kernel(const dg::MeshView m, dg::HalfEdgeRec* he
   const int f = int(s / 3), k = int(s % 3);
   const HalfEdgeRec r = make_halfedge_rec(m, f, k);
   he[s] = r;
+}
+
+// Tensor map of the crossing records for the TMA tile::gather4 fetch of the fast walker: a 2-D
+// f64 tensor [3 nf rows][16 doubles], box = one row, 128-byte swizzle. The driver entry point is
+// taken through the runtime so that the library does not link libcuda.
+bool encode_record_map(const dg::HalfEdgeRec* he, size_t rows, unsigned char* out128) {
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                               const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap is 128 bytes");
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+    cudaGetLastError();
+    return false;
+  }
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {16, cuuint64_t(rows)}, strides[1] = {sizeof(dg::HalfEdgeRec)};
+  const cuuint32_t box[2] = {16, 1}, estr[2] = {1, 1};
+  const CUresult r = reinterpret_cast<EncodeFn>(fn)(
+      &map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<dg::HalfEdgeRec*>(he), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  memcpy(out128, &map, 128);
+  return true;
 }
 
 __global__ void iota_kernel(int32_t* a, int64_t n) {
@@ -289,12 +317,11 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
     } else if (env && (!strcmp(env, "off") || !strcmp(env, "0"))) {
       cache = false;
     } else {
-      // Measured (profiles/tuning_r1.md, scripts/sweep_cache_policy.py): with crossing records the
-      // fast walker runs at 39-42 Gcross/s from 40 k to 640 k faces (records up to 246 MB, far
-      // beyond the L2) and drops to 19.7 Gcross/s at 1 M faces (384 MB), where the uncached walker
-      // (96 B per face) holds 26-29 Gcross/s: the cliff sits where the records outgrow the 256 MB
-      // reach of the TLB (2 MB pages), not where they outgrow the L2.
-      cache = 3 * F * sizeof(dg::HalfEdgeRec) <= (size_t(250) << 20);
+      // Measured (profiles/tuning_r1.md, scripts/sweep_cache_policy.py): the walker over crossing
+      // records beats the one over face records at every mesh size once the records are gathered
+      // through TMA beyond the load path's TLB reach (250 MB; dg_trace_kernel.cu), so AUTO only guards
+      // capacity.
+      cache = 3 * F * sizeof(dg::HalfEdgeRec) <= (size_t(16) << 30);
     }
   }
   if (cache) {
@@ -315,6 +342,7 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   if (m->he) {
     build_halfedges_kernel<<<unsigned((3 * F + 127) / 128), 128, 0, m->stream>>>(m->view_uncached(), m->he);
     DG_TRY(cudaGetLastError());
+    m->he_map_ok = encode_record_map(m->he, 3 * F, m->he_map);
   }
   DG_TRY(cudaMemcpyAsync(m->fnormal, fnormal, 3 * F * sizeof(double), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(m->vangle, vangle, Vn * sizeof(double), cudaMemcpyHostToDevice, m->stream));
@@ -400,7 +428,7 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   DG_CUDA(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, stream));
 
   dg::TraceParams p{};
-  p.mesh = mesh->view();
+  mesh->bind(p);
   p.n = n;
   auto din = [&](int i) { return fin[i].bytes ? dp + fin[i].off : nullptr; };
   auto dout = [&](int i) { return fout[i].bytes ? dp + fout[i].off : nullptr; };
@@ -428,7 +456,7 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   p.want_q = c.want_transport_matrix;
   if (p.total_crossings) DG_CUDA(cudaMemsetAsync(p.total_crossings, 0, 8, stream));
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || out->payload || out->transport;
-  DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, needs_full, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm), c.walker == DG_WALKER_GENERIC}, stream));
+  DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, needs_full, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm), int(c.walker)}, stream));
   if (total > out_begin) DG_CUDA(cudaMemcpyAsync(hp + out_begin, dp + out_begin, total - out_begin, cudaMemcpyDeviceToHost, stream));
   DG_CUDA(cudaStreamSynchronize(stream));
   for (auto& f : fout) if (f.bytes) std::memcpy(f.dst, hp + f.off, f.bytes);
@@ -442,7 +470,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   const size_t N = size_t(n);
   auto at = [](auto* ptr, size_t) { return ptr; };
   dg::TraceParams p{};
-  p.mesh = mesh->view();
+  mesh->bind(p);
   p.n = n;
   p.face = st.in(at(in->face, 1), N);
   p.bary = st.in(at(in->bary, 3), 3 * N);
@@ -496,7 +524,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
 
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || record ||
                           out->payload || out->transport;
-  dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm), c.walker == DG_WALKER_GENERIC};
+  dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm), int(c.walker)};
   st.note(dg::launch_trace(p, c.use_f32 != 0, needs_full, shape, stream));
   if (total_dst) {
     st.note(cudaMemcpyAsync(total_dst, ctr + 1, sizeof(uint64_t),

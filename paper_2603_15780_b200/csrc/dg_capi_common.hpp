@@ -24,6 +24,8 @@ struct dg_mesh {
   int32_t nf = 0, nv = 0;
   dg::FaceRec* rec = nullptr;
   dg::HalfEdgeRec* he = nullptr;  // transport cache (null when off)
+  alignas(64) unsigned char he_map[128] = {};  // CUtensorMap over `he` for the TMA gather (valid iff he_map_ok)
+  bool he_map_ok = false;
   double* fnormal = nullptr;
   double* vangle = nullptr;
   int32_t* csr_off = nullptr;
@@ -51,6 +53,12 @@ struct dg_mesh {
   // the same mesh without the transport cache (f32 lane: its transports are float arithmetic)
   dg::MeshView view_uncached() const {
     return dg::MeshView{rec, nullptr, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
+  }
+  // binds the mesh (and the tensor map of its crossing records) into a trace request
+  void bind(dg::TraceParams& p) const {
+    p.mesh = view();
+    for (int i = 0; i < 128; ++i) p.he_map[i] = he_map[i];
+    p.he_map_ok = he_map_ok ? 1 : 0;
   }
   unsigned long long* next_counters() const { return counters + 2 * (ring.fetch_add(1) % kRing); }
 };

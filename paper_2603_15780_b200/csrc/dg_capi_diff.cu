@@ -19,7 +19,7 @@ cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const do
                      int max_steps, unsigned long long* total, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   dg::TraceParams p{};
-  p.mesh = mesh->view();
+  mesh->bind(p);
   p.n = n;
   p.face = jf; p.bary = jb; p.dir = jd; p.payload = jp;
   p.o_face = rf; p.o_bary = rb; p.o_dir = rd; p.o_payload = rp; p.o_term = rt; p.o_status = rs;

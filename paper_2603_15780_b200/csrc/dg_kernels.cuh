@@ -12,6 +12,9 @@ namespace dg {
 // pointer may be null. Element i of the schedule is query perm[i] (or i when perm is null);
 // results are always written at the query's own index.
 struct TraceParams {
+  // CUtensorMap of the crossing-record array ([3 nf] rows x 16 doubles, 128-byte swizzle) for the TMA
+  // gather of the fast walker; opaque bytes here so that this header needs no driver API
+  alignas(64) unsigned char he_map[128];
   MeshView mesh;
   int64_t n;
   const int32_t* face;
@@ -41,12 +44,13 @@ struct TraceParams {
   int32_t refill_min;  // refill a warp once this many lanes are idle (0 = the walker's default)
   uint8_t hole_avoidance;
   uint8_t want_q;
+  uint8_t he_map_ok;  // he_map is a valid tensor map of mesh.he
 };
 
 struct LaunchShape {
   int sm_count;
   int blocks_per_sm;  // 0 = use the occupancy query
-  bool generic = false;  // never take the fast walker (cross-checks, measurements)
+  int walker = 0;  // DG_WALKER_*: 0 auto, 1 general walker, 2 fast walker / 256-bit loads, 3 fast walker / TMA gather
 };
 
 // needs_full: any of payload / transport matrix / hole avoidance / polyline is requested.

@@ -157,8 +157,9 @@ cudaError_t launch_one(const TraceParams& p_in, LaunchShape shape, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <bool kCached>
+template <bool kCached, bool kTma>
 cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t stream) {
+  constexpr size_t smem = kTma ? size_t(kFastTmaSmemBytes) : 0;
   TraceParams p = p_in;
   // Start-ups side by side: a warp waits for 4 idle lanes, at most DG_REFILL_PATIENCE (8) transitions.
   // Measured: c2 3.97 -> 3.77 ms, c3 24.46 -> 24.63 ms (profiles/tuning_r1.md).
@@ -168,7 +169,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
     static std::atomic<int> cached_per_sm{0};
     per_sm = cached_per_sm.load(std::memory_order_relaxed);
     if (per_sm <= 0) {
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached>, DG_FAST_BLOCK, 0);
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma>, DG_FAST_BLOCK, smem);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
       cached_per_sm.store(per_sm, std::memory_order_relaxed);
@@ -178,7 +179,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
   const long long needed = (p.n + DG_FAST_BLOCK - 1) / DG_FAST_BLOCK;
   if (blocks > needed) blocks = needed;
   if (blocks < 1) blocks = 1;
-  trace_fast_kernel<kCached><<<unsigned(blocks), DG_FAST_BLOCK, 0, stream>>>(p);
+  trace_fast_kernel<kCached, kTma><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -191,6 +192,17 @@ bool fast_walk_enabled() {
   return on;
 }
 
+// The crossing records are gathered with 256-bit loads while they fit the load path's TLB reach
+// and with one TMA bulk copy per record beyond (DG_FAST_TMA=0|1 forces either; dg_fast_walk.cuh).
+bool tma_gather(const MeshView& m) {
+  static const int forced = [] {
+    const char* e = getenv("DG_FAST_TMA");
+    return e ? (!strcmp(e, "0") || !strcmp(e, "off") ? 0 : 1) : -1;
+  }();
+  if (forced >= 0) return forced != 0;
+  return size_t(m.nf) * 3 * sizeof(HalfEdgeRec) > (size_t(250) << 20);
+}
+
 }  // namespace
 
 cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
@@ -199,8 +211,11 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
-  if (!needs_full && !shape.generic && fast_walk_enabled())
-    return p.mesh.he ? launch_fast<true>(p, shape, stream) : launch_fast<false>(p, shape, stream);
+  if (!needs_full && shape.walker != 1 && fast_walk_enabled()) {
+    if (!p.mesh.he) return launch_fast<false, false>(p, shape, stream);
+    const bool tma = p.he_map_ok && (shape.walker == 3 || (shape.walker != 2 && tma_gather(p.mesh)));
+    return tma ? launch_fast<true, true>(p, shape, stream) : launch_fast<true, false>(p, shape, stream);
+  }
   if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
   return needs_full ? launch_one<double, true, false>(p, shape, stream) : launch_one<double, false, false>(p, shape, stream);
 }
@@ -217,7 +232,7 @@ void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm,
   if (use_f32) {
     if (full) query(trace_kernel<float, true, false>, kBlockThreads); else query(trace_kernel<float, false, false>, kBlockThreads);
   } else if (!full && fast_walk_enabled()) {
-    if (cached) query(trace_fast_kernel<true>, DG_FAST_BLOCK); else query(trace_fast_kernel<false>, DG_FAST_BLOCK);
+    if (cached) query(trace_fast_kernel<true, false>, DG_FAST_BLOCK); else query(trace_fast_kernel<false, false>, DG_FAST_BLOCK);
   } else if (cached) {
     if (full) query(trace_kernel<double, true, true>, kBlockThreads); else query(trace_kernel<double, false, true>, kBlockThreads);
   } else {

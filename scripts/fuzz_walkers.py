@@ -57,15 +57,16 @@ def main(rounds=40, n=40000, seed=0):
         max_steps = int(rng.choice([0, 0, 5, 60]))
         ref = None
         for m in meshes:
-            fast = m.trace_batch(f, b, d, max_steps=max_steps)
-            slow = m.trace_batch(f, b, d, max_steps=max_steps, generic_walker=True)
-            for key in FIELDS:
-                x, y = getattr(fast, key), getattr(slow, key)
-                same = (x == y) | ((x != x) & (y != y))
-                if not same.all():
-                    bad += 1
-                    i = np.nonzero(~same.reshape(n, -1).all(1))[0]
-                    print(f"round {r} cache={m.has_transport_cache} scale={scale:g}: {key} differs at {i[:5]} ({len(i)} rows)", flush=True)
+            slow = m.trace_batch(f, b, d, max_steps=max_steps, walker="generic")
+            for walker in (("loads", "tma") if m.has_transport_cache else ("auto",)):
+                fast = m.trace_batch(f, b, d, max_steps=max_steps, walker=walker)
+                for key in FIELDS:
+                    x, y = getattr(fast, key), getattr(slow, key)
+                    same = (x == y) | ((x != x) & (y != y))
+                    if not same.all():
+                        bad += 1
+                        i = np.nonzero(~same.reshape(n, -1).all(1))[0]
+                        print(f"round {r} cache={m.has_transport_cache} walker={walker} scale={scale:g}: {key} differs at {i[:5]} ({len(i)} rows)", flush=True)
             if ref is None:
                 ref = fast
             else:

@@ -1,0 +1,102 @@
+// Micro-benchmark: random 128-byte record gathers from an L2-resident array, one record per lane per
+// iteration, (a) four 256-bit loads per lane, (b) one cp.async.bulk (TMA) per lane into shared memory
+// with a per-warp mbarrier, then eight 128-bit shared loads. Prints records/s per variant.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_bench gather_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ void ldg256(const void* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+__global__ void __launch_bounds__(128, 4) gather_ldg(const char* rec, uint32_t nrec, int iters, double* out) {
+  uint32_t idx = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u % nrec;
+  double acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    const char* p = rec + size_t(idx) * 128;
+    double v[16];
+    ldg256(p, v[0], v[1], v[2], v[3]); ldg256(p + 32, v[4], v[5], v[6], v[7]);
+    ldg256(p + 64, v[8], v[9], v[10], v[11]); ldg256(p + 96, v[12], v[13], v[14], v[15]);
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 15; ++k) s += v[k];
+    acc += s;
+    idx = uint32_t(__double2loint(v[15])) % nrec;   // dependent chain, like the walk
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+constexpr int kStride = 144;  // bytes per lane slot in shared memory (128 + 16: conflict-free 128-bit reads)
+
+__global__ void __launch_bounds__(128, 4) gather_tma(const char* rec, uint32_t nrec, int iters, double* out) {
+  extern __shared__ __align__(128) char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* slot = smem + warp * (32 * kStride) + lane * kStride;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 4 * 32 * kStride) + warp;
+  const uint32_t bar_s = uint32_t(__cvta_generic_to_shared(bar));
+  const uint32_t slot_s = uint32_t(__cvta_generic_to_shared(slot));
+  if (lane == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s));
+  __syncwarp();
+  uint32_t idx = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u % nrec;
+  double acc = 0;
+  uint32_t phase = 0;
+  for (int i = 0; i < iters; ++i) {
+    const char* p = rec + size_t(idx) * 128;
+    if (lane == 0) asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(32 * 128) : "memory");
+    __syncwarp();
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];"
+                 ::"r"(slot_s), "l"(p), "r"(bar_s) : "memory");
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(done) : "r"(bar_s), "r"(phase) : "memory");
+    }
+    phase ^= 1;
+    double s = 0;
+    const double2* q = reinterpret_cast<const double2*>(slot);
+    double2 last;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { double2 t = q[k]; if (k < 7) s += t.x + t.y; else { s += t.x; last = t; } }
+    acc += s;
+    idx = uint32_t(__double2loint(last.y)) % nrec;
+    __syncwarp();   // all lanes have read their slots before the next copies land
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+int main(int argc, char** argv) {
+  const uint32_t nrec = argc > 1 ? atoi(argv[1]) : 245760;   // 31 MB, the c2 record array
+  const int iters = argc > 2 ? atoi(argv[2]) : 2000;
+  char* rec; double* out;
+  cudaMalloc(&rec, size_t(nrec) * 128);
+  // records: 15 doubles of payload + the next index in the low word of the 16th
+  double* h = (double*)malloc(size_t(nrec) * 128);
+  uint32_t x = 12345;
+  for (uint32_t r = 0; r < nrec; ++r) {
+    for (int k = 0; k < 15; ++k) h[size_t(r) * 16 + k] = 1e-3 * k;
+    x = x * 1664525u + 1013904223u;
+    uint64_t bits = x % nrec;
+    memcpy(&h[size_t(r) * 16 + 15], &bits, 8);
+  }
+  cudaMemcpy(rec, h, size_t(nrec) * 128, cudaMemcpyHostToDevice);
+  int sm; cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, 0);
+  const int blocks = sm * 4, threads = 128;
+  cudaMalloc(&out, size_t(blocks) * threads * 8);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const size_t smem = 4 * 32 * kStride + 64;
+  cudaFuncSetAttribute(gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  for (int variant = 0; variant < 2; ++variant) {
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(e0);
+      if (variant == 0) gather_ldg<<<blocks, threads>>>(rec, nrec, iters, out);
+      else gather_tma<<<blocks, threads, smem>>>(rec, nrec, iters, out);
+      cudaEventRecord(e1);
+      cudaError_t err = cudaDeviceSynchronize();
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      if (rep == 2) printf("%s: %.3f ms, %.2f G records/s (%s)\n", variant == 0 ? "4 x LDG.256 per lane" : "1 x cp.async.bulk per lane",
+                           ms, double(blocks) * threads * iters / ms / 1e6, cudaGetErrorString(err));
+    }
+  }
+  return 0;
+}

@@ -15,14 +15,17 @@ FIELDS = ("face", "bary", "dir", "traced", "requested", "term", "status", "stall
 
 
 def both_walkers(m, f, b, d, **kw):
-    fast = m.trace_batch(f, b, d, **kw)
-    slow = m.trace_batch(f, b, d, generic_walker=True, **kw)
-    for k in FIELDS:
-        x, y = getattr(fast, k), getattr(slow, k)
-        same = (x == y) | ((x != x) & (y != y))
-        bad = np.nonzero(~same.reshape(len(f), -1).all(1))[0]
-        assert len(bad) == 0, f"{k}: {len(bad)}/{len(f)} differ, first {bad[:5]}: fast {x[bad[:3]]} generic {y[bad[:3]]}"
-    assert fast.total_crossings == slow.total_crossings == int(slow.crossings.sum())
+    """General walker vs the fast walker with each gather of the crossing records (256-bit loads,
+    TMA tile::gather4; on a mesh without records both selectors run the face-record walker)."""
+    slow = m.trace_batch(f, b, d, walker="generic", **kw)
+    for walker in ("loads", "tma", "auto"):
+        fast = m.trace_batch(f, b, d, walker=walker, **kw)
+        for k in FIELDS:
+            x, y = getattr(fast, k), getattr(slow, k)
+            same = (x == y) | ((x != x) & (y != y))
+            bad = np.nonzero(~same.reshape(len(f), -1).all(1))[0]
+            assert len(bad) == 0, f"{walker} {k}: {len(bad)}/{len(f)} differ, first {bad[:5]}: fast {x[bad[:3]]} generic {y[bad[:3]]}"
+        assert fast.total_crossings == slow.total_crossings == int(slow.crossings.sum())
     return fast
 
 
@@ -102,8 +105,9 @@ def test_rejected_and_degenerate_starts(gpu):
 
 @pytest.mark.parametrize("key,n", [("c2", 60_000), ("c3", 12_000)])
 def test_baseline_configs_against_the_reference(gpu, ref, key, n):
-    """BASELINE.json's meshes at full size (config 2: 81 920 faces with crossing records; config 3:
-    1 M faces, face records only) on a prefix of the benchmark's own query stream: final face,
+    """BASELINE.json's meshes at full size (config 2: 81 920 faces, crossing records gathered with
+    256-bit loads; config 3: 1 M faces, 384 MB of crossing records gathered through TMA
+    tile::gather4) on a prefix of the benchmark's own query stream: final face,
     barycentrics, direction, traced length and the whole face sequence against the UNMODIFIED
     reference -- bit for bit (random starts never take a vertex branch), plus EP gradients."""
     import sys, os
@@ -111,7 +115,7 @@ def test_baseline_configs_against_the_reference(gpu, ref, key, n):
     from bench import make_workload
     xyz, tri, f, b, d, q = make_workload(key, n, 42)
     m = gpu.Mesh(xyz, tri)
-    assert m.has_transport_cache == (key == "c2")
+    assert m.has_transport_cache
     rm = ref.RefMesh.build(xyz, tri)
     ours = both_walkers(m, f, b, d)
     theirs = rm.trace_batch(f, b, d, record_polyline=True)
