@@ -92,11 +92,11 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic():
-    """dram bytes per launch of the trace kernel from the committed ncu capture, if any."""
+def profile_traffic(workload):
+    """dram bytes per launch of the trace kernel from the committed ncu capture of this workload, if any."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
-        return json.load(open(p))
+        return json.load(open(p)).get(workload)
     return None
 
 
@@ -327,8 +327,8 @@ def run_ours(args):
         t_trace = float(np.mean(tr_ms)) * 1e-3
         alg_bytes = crossings_per_step * BYTES_PER_CROSSING + n * BYTES_PER_GEODESIC
         achieved = alg_bytes / t_trace / 1e9
-        traffic = profile_traffic()
-        info = dg.kernel_info(False, False, cached=mesh.has_transport_cache)
+        traffic = profile_traffic(args.workload)
+        info = dg.kernel_info(False, False, cached=mesh.has_transport_cache, tma=mesh.uses_tma_gather)
         line = {"metric": f"face_crossings_per_s_fwd_{scheme}", "value": value, "unit": "face-crossings/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -340,7 +340,9 @@ def run_ours(args):
                                  "geodesics_per_s": n / t_trace},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
-                             "kernel": "trace_fast_kernel<cached>" if mesh.has_transport_cache else "trace_fast_kernel<uncached>",
+                             "kernel": ("trace_fast_kernel<crossing records, TMA tile::gather4>" if mesh.uses_tma_gather else
+                                        "trace_fast_kernel<crossing records, 256-bit loads>" if mesh.has_transport_cache else
+                                        "trace_fast_kernel<face records>"),
                              "peak_source": peak_src,
                              "algorithmic_bytes_per_launch": alg_bytes,
                              "note": "dependent-gather walk: bound by FP64 issue + L2 latency, not HBM bandwidth (DESIGN.md)",

@@ -108,8 +108,9 @@ DG_API int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int
 /* Same, with layout flags. The transport cache stores one 128-byte crossing record per directed
  * half-edge: the fold isometry of tracer.cpp:113-126 plus the two corner-0 edge vectors of the
  * entered face (computed on the device at upload by the same code the uncached walker runs, so
- * results are bit-identical). AUTO enables it while the records stay within 250 MB (about 650 k
- * faces) -- beyond that they outgrow the TLB reach and the uncached walker is faster; env
+ * results are bit-identical). AUTO enables it while the records stay within 16 GB (about 40 M
+ * faces): the fast walker gathers them with 256-bit loads up to 250 MB and through TMA
+ * tile::gather4 beyond (the load path falls off its TLB reach there). Env
  * DG_TRANSPORT_CACHE=on|off overrides AUTO. */
 enum { DG_MESH_TRANSPORT_AUTO = 0, DG_MESH_TRANSPORT_ON = 1, DG_MESH_TRANSPORT_OFF = 2 };
 DG_API int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf,
@@ -117,6 +118,9 @@ DG_API int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, 
                              const uint8_t* vboundary, const int32_t* csr_off,
                              const int32_t* csr_list, uint32_t flags, dg_mesh** out);
 DG_API int dg_mesh_has_transport_cache(const dg_mesh* m);
+/* 1 when the fast walker fetches this mesh's crossing records through TMA tile::gather4 (records
+ * beyond 250 MB), 0 when it gathers them with 256-bit loads or the mesh has none. */
+DG_API int dg_mesh_uses_tma_gather(const dg_mesh* m);
 DG_API void dg_mesh_destroy(dg_mesh* m);
 DG_API int32_t dg_mesh_face_count(const dg_mesh* m);
 DG_API int32_t dg_mesh_vertex_count(const dg_mesh* m);
@@ -183,7 +187,8 @@ DG_API int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in,
                           const dg_trace_cfg* cfg, dg_trace_out* out);
 
 /* Registers per thread, resident CTAs per SM and CTA size of a tracer kernel variant.
- * full: bit 0 = payload / transport matrix / hole avoidance / polyline support compiled in,
+ * full: bit 2 = the TMA-gather variant of the fast walker,
+ *       bit 0 = payload / transport matrix / hole avoidance / polyline support compiled in,
  *       bit 1 = transport-cache variant. */
 DG_API void dg_trace_kernel_info(int use_f32, int full, int* regs, int* blocks_per_sm,
                                  int* block_threads);

@@ -63,6 +63,7 @@ class Mesh:
         L = lib()
         self.transport_cache = transport_cache
         self.has_transport_cache = False
+        self.uses_tma_gather = False
         self.xyz = _f64(xyz).reshape(-1, 3)
         self.tri = _i32(tri).reshape(-1, 3)
         nv, nf = len(self.xyz), len(self.tri)
@@ -100,6 +101,7 @@ class Mesh:
                                   flags, C.addressof(h)))
         self.h = h
         self.has_transport_cache = bool(L.dg_mesh_has_transport_cache(h))
+        self.uses_tma_gather = bool(L.dg_mesh_uses_tma_gather(h))
         return self
 
     def __del__(self):
@@ -382,8 +384,8 @@ class Batch:
         return out
 
 
-def kernel_info(use_f32=False, full=False, cached=False):
+def kernel_info(use_f32=False, full=False, cached=False, tma=False):
     regs, bps, bt = C.c_int(0), C.c_int(0), C.c_int(0)
-    lib().dg_trace_kernel_info(int(use_f32), int(full) | (int(cached) << 1), C.addressof(regs), C.addressof(bps),
+    lib().dg_trace_kernel_info(int(use_f32), int(full) | (int(cached) << 1) | (int(tma) << 2), C.addressof(regs), C.addressof(bps),
                                C.addressof(bt))
     return dict(registers=regs.value, blocks_per_sm=bps.value, block_threads=bt.value)

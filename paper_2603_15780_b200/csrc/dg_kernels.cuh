@@ -57,6 +57,9 @@ struct LaunchShape {
 cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
                          cudaStream_t stream);
 
+// Whether the fast walker gathers this mesh's crossing records through TMA (AUTO policy).
+bool fast_walker_uses_tma(const MeshView& m, bool map_ok);
+
 // Kernel attributes for reporting (registers, max resident blocks per SM).
 void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads);
 

@@ -205,6 +205,8 @@ bool tma_gather(const MeshView& m) {
 
 }  // namespace
 
+bool fast_walker_uses_tma(const MeshView& m, bool map_ok) { return m.he && map_ok && fast_walk_enabled() && tma_gather(m); }
+
 cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
                          cudaStream_t stream) {
   if (p.n <= 0) return cudaSuccess;
@@ -223,7 +225,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
 void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads) {
   cudaFuncAttributes a{};
   int per_sm = 0, threads = kBlockThreads;
-  const bool full = variant & 1, cached = (variant & 2) && !use_f32;
+  const bool full = variant & 1, cached = (variant & 2) && !use_f32, tma = (variant & 4) != 0;
   auto query = [&](auto kernel, int block) {
     cudaFuncGetAttributes(&a, kernel);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
@@ -232,7 +234,15 @@ void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm,
   if (use_f32) {
     if (full) query(trace_kernel<float, true, false>, kBlockThreads); else query(trace_kernel<float, false, false>, kBlockThreads);
   } else if (!full && fast_walk_enabled()) {
-    if (cached) query(trace_fast_kernel<true, false>, DG_FAST_BLOCK); else query(trace_fast_kernel<false, false>, DG_FAST_BLOCK);
+    if (cached && tma) {
+      cudaFuncGetAttributes(&a, trace_fast_kernel<true, true>);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<true, true>, DG_FAST_BLOCK, kFastTmaSmemBytes);
+      threads = DG_FAST_BLOCK;
+    } else if (cached) {
+      query(trace_fast_kernel<true, false>, DG_FAST_BLOCK);
+    } else {
+      query(trace_fast_kernel<false, false>, DG_FAST_BLOCK);
+    }
   } else if (cached) {
     if (full) query(trace_kernel<double, true, true>, kBlockThreads); else query(trace_kernel<double, false, true>, kBlockThreads);
   } else {
