@@ -5,8 +5,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_15780_b200 as dg
 from bench import make_workload
 n = 400000
-xyz, tri, f, b, d, q = make_workload("c2", n, 42)
-mesh = dg.Mesh(xyz, tri, device=0)
+key = sys.argv[1] if len(sys.argv) > 1 else "c2"
+cache = {"on": True, "off": False}.get(os.environ.get("TC", "auto"), "auto")
+xyz, tri, f, b, d, q = make_workload(key, n, 42)
+mesh = dg.Mesh(xyz, tri, device=0, transport_cache=cache)
+print(key, "crossing records:", mesh.has_transport_cache)
 dev = torch.device("cuda", 0)
 t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dtype=dt)
 F, B, D, P = t(f, torch.int32), t(b, torch.float64), t(d, torch.float64), t(q, torch.float64)
