@@ -157,7 +157,7 @@ cudaError_t launch_one(const TraceParams& p_in, LaunchShape shape, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <bool kCached, bool kTma>
+template <bool kCached, bool kTma, bool kPay = false>
 cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t stream) {
   constexpr size_t smem = kTma ? size_t(kFastTmaSmemBytes) : 0;
   TraceParams p = p_in;
@@ -169,7 +169,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
     static std::atomic<int> cached_per_sm{0};
     per_sm = cached_per_sm.load(std::memory_order_relaxed);
     if (per_sm <= 0) {
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma>, DG_FAST_BLOCK, smem);
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma, kPay>, DG_FAST_BLOCK, smem);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
       cached_per_sm.store(per_sm, std::memory_order_relaxed);
@@ -179,7 +179,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
   const long long needed = (p.n + DG_FAST_BLOCK - 1) / DG_FAST_BLOCK;
   if (blocks > needed) blocks = needed;
   if (blocks < 1) blocks = 1;
-  trace_fast_kernel<kCached, kTma><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
+  trace_fast_kernel<kCached, kTma, kPay><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -213,10 +213,16 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
+  const bool tma = p.mesh.he && p.he_map_ok && (shape.walker == 3 || (shape.walker != 2 && tma_gather(p.mesh)));
   if (!needs_full && shape.walker != 1 && fast_walk_enabled()) {
     if (!p.mesh.he) return launch_fast<false, false>(p, shape, stream);
-    const bool tma = p.he_map_ok && (shape.walker == 3 || (shape.walker != 2 && tma_gather(p.mesh)));
     return tma ? launch_fast<true, true>(p, shape, stream) : launch_fast<true, false>(p, shape, stream);
+  }
+  // a payload to transport and nothing else of the full variant: the fast walker carries it along
+  const bool payload_only = (p.payload || p.o_payload) && !p.want_q && !p.o_transport && !p.hole_avoidance && !p.poly_offsets;
+  if (payload_only && shape.walker != 1 && fast_walk_enabled()) {
+    if (!p.mesh.he) return launch_fast<false, false, true>(p, shape, stream);
+    return tma ? launch_fast<true, true, true>(p, shape, stream) : launch_fast<true, false, true>(p, shape, stream);
   }
   if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
   return needs_full ? launch_one<double, true, false>(p, shape, stream) : launch_one<double, false, false>(p, shape, stream);

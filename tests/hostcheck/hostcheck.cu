@@ -33,31 +33,33 @@ struct HostMesh {
 
 // The fast walker (csrc/dg_fast_walk.cuh) driven the way trace_fast_kernel drives a lane: lean
 // start-up, fast steps, the generic paths for everything the fast step hands back.
-template <bool kCached>
+template <bool kCached, bool kPay>
 void run_fast(const HostMesh& hm, const TraceParams& p) {
 #pragma omp parallel for schedule(dynamic, 8)
   for (int64_t q = 0; q < p.n; ++q) {
-    FastLane<kCached> L{};
+    FastLane<kCached, kPay> L{};
     const V3<double> qb{p.bary[3 * q], p.bary[3 * q + 1], p.bary[3 * q + 2]};
     const V3<double> qv{p.dir[3 * q], p.dir[3 * q + 1], p.dir[3 * q + 2]};
-    bool live = fast_init<kCached>(p.mesh, p.face[q], qb, qv, L);
+    V3<double> pay{0, 0, 0};
+    if (kPay && p.payload) pay = {p.payload[3 * q], p.payload[3 * q + 1], p.payload[3 * q + 2]};
+    bool live = fast_init<kCached, kPay>(p.mesh, p.face[q], qb, qv, L, pay);
     if (!live) {
       LaneState S;
-      live = lane_init<kCached>(p, q, &S);
-      lane_in<kCached>(p.mesh, S, L);
+      live = lane_init<kCached, kPay>(p, q, &S);
+      lane_in<kCached, kPay>(p.mesh, S, L);
     }
     while (live) {
       StepSpill sp;
-      const int action = fast_step<kCached>(p.mesh, p.max_steps, L, sp);
+      const int action = fast_step<kCached, false, kPay>(p.mesh, p.max_steps, L, sp);
       if (action == kActFast) continue;
       if (action == kActFinish) {
-        fast_finish<kCached>(p, q, L, sp);
+        fast_finish<kCached, kPay>(p, q, L, sp);
         break;
       }
       LaneState S;
-      lane_out<kCached>(L, sp, S);
-      live = lane_generic<kCached>(p, q, &S, action);
-      lane_in<kCached>(p.mesh, S, L);
+      lane_out<kCached, kPay>(L, sp, S);
+      live = lane_generic<kCached, kPay>(p, q, &S, action);
+      lane_in<kCached, kPay>(p.mesh, S, L);
     }
   }
 }
@@ -145,6 +147,7 @@ HC_API void hc_trace_batch(void* h, int64_t n, const int32_t* face, const double
 // The fast walker on the host, with (cached = 1) or without crossing records. fast_steps (may be
 // null) receives how many transitions the fast step committed, to prove it is the path under test.
 HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const double* bary, const double* dir,
+                                const double* payload, double* o_payload,
                                 int max_steps, int cached, int32_t* o_face, double* o_bary, double* o_dir,
                                 double* o_traced, double* o_requested, uint8_t* o_term, uint8_t* o_status,
                                 uint8_t* o_stall, int32_t* o_npoints, int32_t* o_crossings) {
@@ -162,5 +165,7 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
   p.o_face = o_face; p.o_bary = o_bary; p.o_dir = o_dir; p.o_traced = o_traced; p.o_requested = o_requested;
   p.o_term = o_term; p.o_status = o_status; p.o_stall = o_stall; p.o_npoints = o_npoints; p.o_crossings = o_crossings;
   p.max_steps = max_steps;
-  if (cached) run_fast<true>(hm, p); else run_fast<false>(hm, p);
+  p.payload = payload; p.o_payload = o_payload;
+  if (payload) { if (cached) run_fast<true, true>(hm, p); else run_fast<false, true>(hm, p); }
+  else { if (cached) run_fast<true, false>(hm, p); else run_fast<false, false>(hm, p); }
 }

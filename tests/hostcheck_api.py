@@ -87,10 +87,10 @@ class HostMesh:
             r.has_payload = (np.square(payload).sum(1) > 0).astype(np.uint8)
         return r
 
-    def trace_batch_fast(self, face, bary, dirs, max_steps=0, cached=False):
+    def trace_batch_fast(self, face, bary, dirs, max_steps=0, cached=False, payload=None):
         """The fast walker (csrc/dg_fast_walk.cuh: fast_init / fast_step / fast_finish + the generic
         paths behind them) driven on the host the way trace_fast_kernel drives a lane."""
-        face, bary, dirs = _i32(face), _f64(bary), _f64(dirs)
+        face, bary, dirs, payload = _i32(face), _f64(bary), _f64(dirs), _f64(payload)
         n = len(face)
         if max_steps <= 0:
             max_steps = int(10.0 * np.sqrt(float(self.nf))) + 100
@@ -99,7 +99,10 @@ class HostMesh:
                         status=np.empty(n, np.uint8), npoints=np.empty(n, np.int32))
         r.stall = np.empty(n, np.uint8)
         r.crossings = np.empty(n, np.int32)
-        lib().hc_trace_batch_fast(self.h, C.c_int64(n), _p(face), _p(bary), _p(dirs), int(max_steps), int(cached),
+        if payload is not None:
+            r.payload = np.empty((n, 3))
+        lib().hc_trace_batch_fast(self.h, C.c_int64(n), _p(face), _p(bary), _p(dirs), _p(payload), _p(r.payload),
+                                  int(max_steps), int(cached),
                                   _p(r.face), _p(r.bary), _p(r.dir), _p(r.traced), _p(r.requested), _p(r.term),
                                   _p(r.status), _p(r.stall), _p(r.npoints), _p(r.crossings))
         return r

@@ -30,6 +30,38 @@ def both_walkers(m, f, b, d, **kw):
 
 
 @pytest.mark.parametrize("cache", [True, False])
+def test_payload_lane_of_the_fast_walker(gpu, ref, cache):
+    """A payload to transport and nothing else of the full variant runs on the fast walker (kPay):
+    transported payload and end states bit-identical to the general walker with every gather, on
+    closed and open meshes, with payload-free (zero) elements, vertex starts and a tight step
+    limit; and bit-identical to the reference where no vertex branch is taken."""
+    rng = np.random.default_rng(8)
+    for rm, seed, max_steps in ((ref.RefMesh.icosphere(4), 41, 0), (ref.RefMesh.torus(1 / 3, 1 / 6, 60, 30), 42, 0),
+                                (ref.RefMesh.plane(12, 9, 1.0, 2), 43, 0), (ref.RefMesh.icosphere(3), 44, 11)):
+        a = rm.arrays()
+        m = gpu.Mesh(a["xyz"], a["tri"], transport_cache=cache)
+        f, b, d = rm.sample_queries(seed, 12000, 0.05, 2.5)
+        pay = rng.normal(size=(len(f), 3)) * 10.0 ** rng.uniform(-3, 3, (len(f), 1))
+        pay[::7] = 0.0                      # zero payload = no payload (tracer.cpp:580-583)
+        b[100:200] = [0.0, 1.0, 0.0]        # vertex starts: the generic path carries the payload over the fan
+        slow = m.trace_batch(f, b, d, payload=pay, max_steps=max_steps, walker="generic")
+        for walker in ("loads", "tma", "auto"):
+            fast = m.trace_batch(f, b, d, payload=pay, max_steps=max_steps, walker=walker)
+            for k in FIELDS + ("payload",):
+                x, y = getattr(fast, k), getattr(slow, k)
+                assert np.array_equal(x, y, equal_nan=True), (walker, k)
+        theirs = rm.trace_batch(f, b, d, payload=pay, max_steps=max_steps, record_polyline=True)
+        no_vertex = np.ones(len(f), bool)
+        at_vertex = (theirs.poly_bary == 1.0).any(1)
+        np.logical_and.at(no_vertex, np.repeat(np.arange(len(f)), np.diff(theirs.poly_offsets)), ~at_vertex)
+        assert np.array_equal(fast.face, theirs.face) and np.array_equal(fast.term, theirs.term)
+        assert np.array_equal(fast.payload[no_vertex], theirs.payload[no_vertex])
+        assert np.abs(fast.payload - theirs.payload).max() <= 1e-9 * np.abs(pay).max()
+        keep = np.linalg.norm(pay, axis=1) > 0
+        assert np.abs(np.linalg.norm(fast.payload[keep], axis=1) / np.linalg.norm(pay[keep], axis=1) - 1).max() < 1e-10
+
+
+@pytest.mark.parametrize("cache", [True, False])
 def test_bumpy_sphere_config2_style(gpu, cache):
     xyz, tri = W.bumpy_sphere(5)
     m = gpu.Mesh(xyz, tri, transport_cache=cache)

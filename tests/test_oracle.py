@@ -83,18 +83,22 @@ def test_fast_walker_on_host_matches_fixtures(hostcheck, oracle, path, cached):
     """The fast walker (csrc/dg_fast_walk.cuh: lean start-up, fast step, finish, and the generic
     paths it hands everything else to) compiled for the host and driven the way the kernel drives
     a lane: end states and counters of the reference fixtures, bit for bit, on both mesh layouts.
-    (A payload or a transport matrix rides along without changing the path, so those fixtures pin
-    the fast walker's end states too; hole avoidance changes the path and belongs to the general
-    walker only.)"""
+    (Fixtures with a payload run the payload lane of the fast walker and pin the transported
+    payload as well; a transport matrix rides along without changing the path; hole avoidance
+    changes the path and belongs to the general walker only.)"""
     z = np.load(path)
     if z["cfg"][1]:
         pytest.skip("hole avoidance: general walker")
     a = oracle.OracleMesh(z["xyz"], z["tri"]).arrays()
     hm = hostcheck.HostMesh(a)
-    r = hm.trace_batch_fast(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), cached=cached)
+    pay = z["payload"] if z["payload"].size else None
+    r = hm.trace_batch_fast(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), cached=cached, payload=pay)
     for k in ("face", "term", "status", "npoints"):
         assert np.array_equal(z["o_" + k], getattr(r, k)), k
-    for k, got in (("o_bary", r.bary), ("o_dir", r.dir), ("o_traced", r.traced), ("o_requested", r.requested)):
+    pairs = [("o_bary", r.bary), ("o_dir", r.dir), ("o_traced", r.traced), ("o_requested", r.requested)]
+    if pay is not None:
+        pairs.append(("o_payload", r.payload))   # the payload lane of the fast walker (kPay)
+    for k, got in pairs:
         assert _equal(z[k], got), f"{k} not bit-equal"
     g = hm.trace_batch(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]))
     assert np.array_equal(g.crossings, r.crossings) and np.array_equal(g.stall, r.stall)
