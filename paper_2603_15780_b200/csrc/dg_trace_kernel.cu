@@ -218,8 +218,9 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
     if (!p.mesh.he) return launch_fast<false, false>(p, shape, stream);
     return tma ? launch_fast<true, true>(p, shape, stream) : launch_fast<true, false>(p, shape, stream);
   }
-  // a payload to transport and nothing else of the full variant: the fast walker carries it along
-  const bool payload_only = (p.payload || p.o_payload) && !p.want_q && !p.o_transport && !p.hole_avoidance && !p.poly_offsets;
+  // a payload to transport and / or hole avoidance, but no transport matrix and no polyline: the fast
+  // walker carries the payload along and leaves boundary events to the full Tracer behind it
+  const bool payload_only = (p.payload || p.o_payload || p.hole_avoidance) && !p.want_q && !p.o_transport && !p.poly_offsets;
   if (payload_only && shape.walker != 1 && fast_walk_enabled()) {
     if (!p.mesh.he) return launch_fast<false, false, true>(p, shape, stream);
     return tma ? launch_fast<true, true, true>(p, shape, stream) : launch_fast<true, false, true>(p, shape, stream);

@@ -147,7 +147,7 @@ HC_API void hc_trace_batch(void* h, int64_t n, const int32_t* face, const double
 // The fast walker on the host, with (cached = 1) or without crossing records. fast_steps (may be
 // null) receives how many transitions the fast step committed, to prove it is the path under test.
 HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const double* bary, const double* dir,
-                                const double* payload, double* o_payload,
+                                const double* payload, double* o_payload, int hole,
                                 int max_steps, int cached, int32_t* o_face, double* o_bary, double* o_dir,
                                 double* o_traced, double* o_requested, uint8_t* o_term, uint8_t* o_status,
                                 uint8_t* o_stall, int32_t* o_npoints, int32_t* o_crossings) {
@@ -166,6 +166,7 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
   p.o_term = o_term; p.o_status = o_status; p.o_stall = o_stall; p.o_npoints = o_npoints; p.o_crossings = o_crossings;
   p.max_steps = max_steps;
   p.payload = payload; p.o_payload = o_payload;
-  if (payload) { if (cached) run_fast<true, true>(hm, p); else run_fast<false, true>(hm, p); }
+  p.hole_avoidance = uint8_t(hole != 0);
+  if (payload || hole) { if (cached) run_fast<true, true>(hm, p); else run_fast<false, true>(hm, p); }
   else { if (cached) run_fast<true, false>(hm, p); else run_fast<false, false>(hm, p); }
 }

@@ -62,6 +62,33 @@ def test_payload_lane_of_the_fast_walker(gpu, ref, cache):
 
 
 @pytest.mark.parametrize("cache", [True, False])
+def test_hole_avoidance_on_the_fast_walker(gpu, ref, cache):
+    """hole_avoidance requests (without polyline / transport matrix) run on the fast walker with
+    the full Tracer behind it: boundary edges and boundary vertices -- where hole avoidance acts --
+    are exactly what the fast step hands over. Bit-identical to the general walker, with and
+    without a payload; end states equal to the reference."""
+    rng = np.random.default_rng(9)
+    for rm, seed in ((ref.RefMesh.plane(10, 7, 1.0, 4), 51), (ref.RefMesh.cylinder(0.5, 1.5, 20, 6), 52),
+                     (ref.RefMesh.icosphere(3), 53)):
+        a = rm.arrays()
+        m = gpu.Mesh(a["xyz"], a["tri"], transport_cache=cache)
+        f, b, d = rm.sample_queries(seed, 8000, 0.1, 4.0)
+        pay = rng.normal(size=(len(f), 3))
+        for kw in (dict(), dict(payload=pay)):
+            slow = m.trace_batch(f, b, d, hole_avoidance=True, walker="generic", **kw)
+            for walker in ("loads", "tma", "auto"):
+                fast = m.trace_batch(f, b, d, hole_avoidance=True, walker=walker, **kw)
+                for k in FIELDS + (("payload",) if kw else ()):
+                    assert np.array_equal(getattr(fast, k), getattr(slow, k), equal_nan=True), (walker, k)
+            theirs = rm.trace_batch(f, b, d, hole_avoidance=True, record_polyline=True, **kw)
+            assert np.array_equal(fast.face, theirs.face) and np.array_equal(fast.term, theirs.term)
+            assert np.abs(fast.bary - theirs.bary).max() < 1e-9 and np.abs(fast.traced - theirs.traced).max() < 1e-9
+        if a["vboundary"].any():
+            plain = m.trace_batch(f, b, d)
+            assert (plain.term == 1).any() and (fast.term == 0).all()   # what stopped at the boundary now slides along it
+
+
+@pytest.mark.parametrize("cache", [True, False])
 def test_bumpy_sphere_config2_style(gpu, cache):
     xyz, tri = W.bumpy_sphere(5)
     m = gpu.Mesh(xyz, tri, transport_cache=cache)

@@ -84,15 +84,14 @@ def test_fast_walker_on_host_matches_fixtures(hostcheck, oracle, path, cached):
     paths it hands everything else to) compiled for the host and driven the way the kernel drives
     a lane: end states and counters of the reference fixtures, bit for bit, on both mesh layouts.
     (Fixtures with a payload run the payload lane of the fast walker and pin the transported
-    payload as well; a transport matrix rides along without changing the path; hole avoidance
-    changes the path and belongs to the general walker only.)"""
+    payload as well; hole-avoidance fixtures run it with the full Tracer behind the fast step; a
+    transport matrix rides along without changing the path.)"""
     z = np.load(path)
-    if z["cfg"][1]:
-        pytest.skip("hole avoidance: general walker")
     a = oracle.OracleMesh(z["xyz"], z["tri"]).arrays()
     hm = hostcheck.HostMesh(a)
     pay = z["payload"] if z["payload"].size else None
-    r = hm.trace_batch_fast(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), cached=cached, payload=pay)
+    r = hm.trace_batch_fast(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), cached=cached, payload=pay,
+                            hole_avoidance=bool(z["cfg"][1]))
     for k in ("face", "term", "status", "npoints"):
         assert np.array_equal(z["o_" + k], getattr(r, k)), k
     pairs = [("o_bary", r.bary), ("o_dir", r.dir), ("o_traced", r.traced), ("o_requested", r.requested)]
@@ -100,7 +99,7 @@ def test_fast_walker_on_host_matches_fixtures(hostcheck, oracle, path, cached):
         pairs.append(("o_payload", r.payload))   # the payload lane of the fast walker (kPay)
     for k, got in pairs:
         assert _equal(z[k], got), f"{k} not bit-equal"
-    g = hm.trace_batch(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]))
+    g = hm.trace_batch(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), hole_avoidance=bool(z["cfg"][1]))
     assert np.array_equal(g.crossings, r.crossings) and np.array_equal(g.stall, r.stall)
 
 
