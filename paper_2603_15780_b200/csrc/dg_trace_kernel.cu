@@ -218,9 +218,10 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
     if (!p.mesh.he) return launch_fast<false, false>(p, shape, stream);
     return tma ? launch_fast<true, true>(p, shape, stream) : launch_fast<true, false>(p, shape, stream);
   }
-  // a payload to transport and / or hole avoidance, but no transport matrix and no polyline: the fast
-  // walker carries the payload along and leaves boundary events to the full Tracer behind it
-  const bool payload_only = (p.payload || p.o_payload || p.hole_avoidance) && !p.want_q && !p.o_transport && !p.poly_offsets;
+  // a payload to transport, hole avoidance, a polyline to record -- anything but the transport matrix:
+  // the fast walker carries the payload along, writes one polyline point per step and leaves boundary
+  // events to the full Tracer behind it
+  const bool payload_only = (p.payload || p.o_payload || p.hole_avoidance || p.poly_offsets) && !p.want_q && !p.o_transport;
   if (payload_only && shape.walker != 1 && fast_walk_enabled()) {
     if (!p.mesh.he) return launch_fast<false, false, true>(p, shape, stream);
     return tma ? launch_fast<true, true, true>(p, shape, stream) : launch_fast<true, false, true>(p, shape, stream);

@@ -38,11 +38,7 @@ void run_fast(const HostMesh& hm, const TraceParams& p) {
 #pragma omp parallel for schedule(dynamic, 8)
   for (int64_t q = 0; q < p.n; ++q) {
     FastLane<kCached, kPay> L{};
-    const V3<double> qb{p.bary[3 * q], p.bary[3 * q + 1], p.bary[3 * q + 2]};
-    const V3<double> qv{p.dir[3 * q], p.dir[3 * q + 1], p.dir[3 * q + 2]};
-    V3<double> pay{0, 0, 0};
-    if (kPay && p.payload) pay = {p.payload[3 * q], p.payload[3 * q + 1], p.payload[3 * q + 2]};
-    bool live = fast_init<kCached, kPay>(p.mesh, p.face[q], qb, qv, L, pay);
+    bool live = fast_init<kCached, kPay>(p, q, L);
     if (!live) {
       LaneState S;
       live = lane_init<kCached, kPay>(p, q, &S);
@@ -50,7 +46,7 @@ void run_fast(const HostMesh& hm, const TraceParams& p) {
     }
     while (live) {
       StepSpill sp;
-      const int action = fast_step<kCached, false, kPay>(p.mesh, p.max_steps, L, sp);
+      const int action = fast_step<kCached, false, kPay>(p, L, sp);
       if (action == kActFast) continue;
       if (action == kActFinish) {
         fast_finish<kCached, kPay>(p, q, L, sp);
@@ -150,7 +146,8 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
                                 const double* payload, double* o_payload, int hole,
                                 int max_steps, int cached, int32_t* o_face, double* o_bary, double* o_dir,
                                 double* o_traced, double* o_requested, uint8_t* o_term, uint8_t* o_status,
-                                uint8_t* o_stall, int32_t* o_npoints, int32_t* o_crossings) {
+                                uint8_t* o_stall, int32_t* o_npoints, int32_t* o_crossings, const int64_t* poly_off,
+                                int32_t* pf, double* pb, double* ps) {
   HostMesh& hm = *static_cast<HostMesh*>(h);
   if (cached && hm.he.empty()) {
     hm.he.resize(3 * size_t(hm.nf));
@@ -167,6 +164,7 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
   p.max_steps = max_steps;
   p.payload = payload; p.o_payload = o_payload;
   p.hole_avoidance = uint8_t(hole != 0);
-  if (payload || hole) { if (cached) run_fast<true, true>(hm, p); else run_fast<false, true>(hm, p); }
+  p.poly_offsets = poly_off; p.poly_face = pf; p.poly_bary = pb; p.poly_seg = ps;
+  if (payload || hole || poly_off) { if (cached) run_fast<true, true>(hm, p); else run_fast<false, true>(hm, p); }
   else { if (cached) run_fast<true, false>(hm, p); else run_fast<false, false>(hm, p); }
 }

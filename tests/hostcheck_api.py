@@ -87,7 +87,8 @@ class HostMesh:
             r.has_payload = (np.square(payload).sum(1) > 0).astype(np.uint8)
         return r
 
-    def trace_batch_fast(self, face, bary, dirs, max_steps=0, cached=False, payload=None, hole_avoidance=False):
+    def trace_batch_fast(self, face, bary, dirs, max_steps=0, cached=False, payload=None, hole_avoidance=False,
+                         record_polyline=False):
         """The fast walker (csrc/dg_fast_walk.cuh: fast_init / fast_step / fast_finish + the generic
         paths behind them) driven on the host the way trace_fast_kernel drives a lane."""
         face, bary, dirs, payload = _i32(face), _f64(bary), _f64(dirs), _f64(payload)
@@ -101,8 +102,20 @@ class HostMesh:
         r.crossings = np.empty(n, np.int32)
         if payload is not None:
             r.payload = np.empty((n, 3))
-        lib().hc_trace_batch_fast(self.h, C.c_int64(n), _p(face), _p(bary), _p(dirs), _p(payload), _p(r.payload),
-                                  int(hole_avoidance), int(max_steps), int(cached),
-                                  _p(r.face), _p(r.bary), _p(r.dir), _p(r.traced), _p(r.requested), _p(r.term),
-                                  _p(r.status), _p(r.stall), _p(r.npoints), _p(r.crossings))
+
+        def call(off, pf, pb, ps):
+            lib().hc_trace_batch_fast(self.h, C.c_int64(n), _p(face), _p(bary), _p(dirs), _p(payload), _p(r.payload),
+                                      int(hole_avoidance), int(max_steps), int(cached), _p(r.face), _p(r.bary), _p(r.dir),
+                                      _p(r.traced), _p(r.requested), _p(r.term), _p(r.status), _p(r.stall), _p(r.npoints),
+                                      _p(r.crossings), _p(off), _p(pf), _p(pb), _p(ps))
+        call(None, None, None, None)
+        if record_polyline:   # the two passes of the C-ABI: count, scan, fill
+            off = np.zeros(n + 1, np.int64)
+            np.cumsum(r.npoints, out=off[1:])
+            tot = int(off[-1])
+            r.poly_offsets = off
+            r.poly_face = np.empty(tot, np.int32)
+            r.poly_bary = np.empty((tot, 3))
+            r.poly_seg = np.empty(tot)
+            call(off, r.poly_face, r.poly_bary, r.poly_seg)
         return r

@@ -91,7 +91,9 @@ def test_fast_walker_on_host_matches_fixtures(hostcheck, oracle, path, cached):
     hm = hostcheck.HostMesh(a)
     pay = z["payload"] if z["payload"].size else None
     r = hm.trace_batch_fast(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), cached=cached, payload=pay,
-                            hole_avoidance=bool(z["cfg"][1]))
+                            hole_avoidance=bool(z["cfg"][1]), record_polyline=True)
+    assert np.array_equal(z["poly_face"], r.poly_face), "face sequence"
+    assert _equal(z["poly_bary"], r.poly_bary) and _equal(z["poly_seg"], r.poly_seg)
     for k in ("face", "term", "status", "npoints"):
         assert np.array_equal(z["o_" + k], getattr(r, k)), k
     pairs = [("o_bary", r.bary), ("o_dir", r.dir), ("o_traced", r.traced), ("o_requested", r.requested)]
