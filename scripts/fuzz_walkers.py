@@ -67,6 +67,18 @@ def main(rounds=40, n=40000, seed=0):
                         bad += 1
                         i = np.nonzero(~same.reshape(n, -1).all(1))[0]
                         print(f"round {r} cache={m.has_transport_cache} walker={walker} scale={scale:g}: {key} differs at {i[:5]} ({len(i)} rows)", flush=True)
+            # the full-Tracer-backed variant: payload + hole avoidance + polylines in one request
+            pay = rng.normal(size=(n, 3)) * scale
+            pay[::5] = 0.0
+            kw = dict(max_steps=max_steps, payload=pay, hole_avoidance=bool(r % 2), record_polyline=True)
+            slow_full = m.trace_batch(f, b, d, walker="generic", **kw)
+            for walker in (("loads", "tma") if m.has_transport_cache else ("auto",)):
+                fast_full = m.trace_batch(f, b, d, walker=walker, **kw)
+                for key in FIELDS + ("payload", "poly_face", "poly_bary", "poly_seg"):
+                    x, y = getattr(fast_full, key), getattr(slow_full, key)
+                    if not np.array_equal(x, y, equal_nan=True):
+                        bad += 1
+                        print(f"round {r} cache={m.has_transport_cache} walker={walker} scale={scale:g}: full-variant {key} differs", flush=True)
             if ref is None:
                 ref = fast
             else:
