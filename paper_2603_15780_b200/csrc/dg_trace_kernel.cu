@@ -157,7 +157,7 @@ cudaError_t launch_one(const TraceParams& p_in, LaunchShape shape, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <bool kCached, bool kTma, bool kPay = false>
+template <bool kCached, bool kTma, int kPay = 0>
 cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t stream) {
   constexpr size_t smem = kTma ? size_t(kFastTmaSmemBytes) : 0;
   TraceParams p = p_in;
@@ -223,8 +223,13 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   // events to the full Tracer behind it
   const bool payload_only = (p.payload || p.o_payload || p.hole_avoidance || p.poly_offsets) && !p.want_q && !p.o_transport;
   if (payload_only && shape.walker != 1 && fast_walk_enabled()) {
-    if (!p.mesh.he) return launch_fast<false, false, true>(p, shape, stream);
-    return tma ? launch_fast<true, true, true>(p, shape, stream) : launch_fast<true, false, true>(p, shape, stream);
+    if (!p.mesh.he) return launch_fast<false, false, 1>(p, shape, stream);
+    return tma ? launch_fast<true, true, 1>(p, shape, stream) : launch_fast<true, false, 1>(p, shape, stream);
+  }
+  // the transport matrix as well: three more vectors through every fold isometry
+  if (p.want_q && shape.walker != 1 && fast_walk_enabled()) {
+    if (!p.mesh.he) return launch_fast<false, false, 2>(p, shape, stream);
+    return tma ? launch_fast<true, true, 2>(p, shape, stream) : launch_fast<true, false, 2>(p, shape, stream);
   }
   if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
   return needs_full ? launch_one<double, true, false>(p, shape, stream) : launch_one<double, false, false>(p, shape, stream);

@@ -33,7 +33,7 @@ struct HostMesh {
 
 // The fast walker (csrc/dg_fast_walk.cuh) driven the way trace_fast_kernel drives a lane: lean
 // start-up, fast steps, the generic paths for everything the fast step hands back.
-template <bool kCached, bool kPay>
+template <bool kCached, int kPay>
 void run_fast(const HostMesh& hm, const TraceParams& p) {
 #pragma omp parallel for schedule(dynamic, 8)
   for (int64_t q = 0; q < p.n; ++q) {
@@ -143,7 +143,7 @@ HC_API void hc_trace_batch(void* h, int64_t n, const int32_t* face, const double
 // The fast walker on the host, with (cached = 1) or without crossing records. fast_steps (may be
 // null) receives how many transitions the fast step committed, to prove it is the path under test.
 HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const double* bary, const double* dir,
-                                const double* payload, double* o_payload, int hole,
+                                const double* payload, double* o_payload, int hole, int want_q, double* o_q,
                                 int max_steps, int cached, int32_t* o_face, double* o_bary, double* o_dir,
                                 double* o_traced, double* o_requested, uint8_t* o_term, uint8_t* o_status,
                                 uint8_t* o_stall, int32_t* o_npoints, int32_t* o_crossings, const int64_t* poly_off,
@@ -165,6 +165,8 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
   p.payload = payload; p.o_payload = o_payload;
   p.hole_avoidance = uint8_t(hole != 0);
   p.poly_offsets = poly_off; p.poly_face = pf; p.poly_bary = pb; p.poly_seg = ps;
-  if (payload || hole || poly_off) { if (cached) run_fast<true, true>(hm, p); else run_fast<false, true>(hm, p); }
-  else { if (cached) run_fast<true, false>(hm, p); else run_fast<false, false>(hm, p); }
+  p.want_q = uint8_t(want_q != 0); p.o_transport = o_q;
+  if (want_q) { if (cached) run_fast<true, 2>(hm, p); else run_fast<false, 2>(hm, p); }
+  else if (payload || hole || poly_off) { if (cached) run_fast<true, 1>(hm, p); else run_fast<false, 1>(hm, p); }
+  else { if (cached) run_fast<true, 0>(hm, p); else run_fast<false, 0>(hm, p); }
 }

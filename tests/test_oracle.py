@@ -84,14 +84,14 @@ def test_fast_walker_on_host_matches_fixtures(hostcheck, oracle, path, cached):
     paths it hands everything else to) compiled for the host and driven the way the kernel drives
     a lane: end states and counters of the reference fixtures, bit for bit, on both mesh layouts.
     (Fixtures with a payload run the payload lane of the fast walker and pin the transported
-    payload as well; hole-avoidance fixtures run it with the full Tracer behind the fast step; a
-    transport matrix rides along without changing the path.)"""
+    payload as well; hole-avoidance fixtures run it with the full Tracer behind the fast step;
+    transport-matrix fixtures run the variant that carries the three matrix columns.)"""
     z = np.load(path)
     a = oracle.OracleMesh(z["xyz"], z["tri"]).arrays()
     hm = hostcheck.HostMesh(a)
     pay = z["payload"] if z["payload"].size else None
     r = hm.trace_batch_fast(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), cached=cached, payload=pay,
-                            hole_avoidance=bool(z["cfg"][1]), record_polyline=True)
+                            hole_avoidance=bool(z["cfg"][1]), record_polyline=True, want_q=bool(z["cfg"][2]))
     assert np.array_equal(z["poly_face"], r.poly_face), "face sequence"
     assert _equal(z["poly_bary"], r.poly_bary) and _equal(z["poly_seg"], r.poly_seg)
     for k in ("face", "term", "status", "npoints"):
@@ -99,6 +99,8 @@ def test_fast_walker_on_host_matches_fixtures(hostcheck, oracle, path, cached):
     pairs = [("o_bary", r.bary), ("o_dir", r.dir), ("o_traced", r.traced), ("o_requested", r.requested)]
     if pay is not None:
         pairs.append(("o_payload", r.payload))   # the payload lane of the fast walker (kPay)
+    if z["cfg"][2]:
+        pairs.append(("o_q", r.q))               # the transport-matrix lane (kPay == 2)
     for k, got in pairs:
         assert _equal(z[k], got), f"{k} not bit-equal"
     g = hm.trace_batch(z["face"], z["bary"], z["dir"], max_steps=int(z["cfg"][0]), hole_avoidance=bool(z["cfg"][1]))
