@@ -79,6 +79,18 @@ def main(rounds=40, n=40000, seed=0):
                     if not np.array_equal(x, y, equal_nan=True):
                         bad += 1
                         print(f"round {r} cache={m.has_transport_cache} walker={walker} scale={scale:g}: full-variant {key} differs", flush=True)
+            # the transport-matrix lane (kPay = 2), with and without a payload, with and without polylines
+            kw = dict(max_steps=max_steps, want_q=True, hole_avoidance=bool((r >> 1) % 2), record_polyline=bool(r % 3 == 0))
+            if r % 2:
+                kw["payload"] = pay
+            slow_q = m.trace_batch(f, b, d, walker="generic", **kw)
+            for walker in (("loads", "tma") if m.has_transport_cache else ("auto",)):
+                fast_q = m.trace_batch(f, b, d, walker=walker, **kw)
+                keys = FIELDS + ("q",) + (("payload",) if r % 2 else ()) + (("poly_face", "poly_bary", "poly_seg") if r % 3 == 0 else ())
+                for key in keys:
+                    if not np.array_equal(getattr(fast_q, key), getattr(slow_q, key), equal_nan=True):
+                        bad += 1
+                        print(f"round {r} cache={m.has_transport_cache} walker={walker} scale={scale:g}: transport-matrix variant {key} differs", flush=True)
             if ref is None:
                 ref = fast
             else:

@@ -62,6 +62,45 @@ def test_payload_lane_of_the_fast_walker(gpu, ref, cache):
 
 
 @pytest.mark.parametrize("cache", [True, False])
+def test_transport_matrix_lane_of_the_fast_walker(gpu, ref, cache):
+    """want_transport_matrix requests (tracer.cpp:99-102, the opt.cpp:298-323 use) run on the fast
+    walker's kPay = 2 lane: Q, payload and end states bit-identical to the general walker with
+    every gather, on closed and open meshes, with vertex starts, hole avoidance and a tight step
+    limit; bit-identical to the reference where no vertex branch is taken; Q stays an isometry of
+    the tangent planes (columns of a rotation restricted to the end plane)."""
+    rng = np.random.default_rng(10)
+    for rm, seed, max_steps, hole in ((ref.RefMesh.icosphere(4), 61, 0, False), (ref.RefMesh.torus(1 / 3, 1 / 6, 48, 24), 62, 0, False),
+                                      (ref.RefMesh.plane(11, 8, 1.0, 3), 63, 0, True), (ref.RefMesh.icosphere(3), 64, 9, False)):
+        a = rm.arrays()
+        m = gpu.Mesh(a["xyz"], a["tri"], transport_cache=cache)
+        f, b, d = rm.sample_queries(seed, 9000, 0.05, 2.5)
+        pay = rng.normal(size=(len(f), 3))
+        pay[::6] = 0.0
+        b[50:120] = [0.0, 0.0, 1.0]
+        for kw in (dict(), dict(payload=pay)):
+            kw = dict(kw, want_q=True, max_steps=max_steps, hole_avoidance=hole)
+            slow = m.trace_batch(f, b, d, walker="generic", **kw)
+            for walker in ("loads", "tma", "auto"):
+                fast = m.trace_batch(f, b, d, walker=walker, **kw)
+                for k in FIELDS + ("q",) + (("payload",) if "payload" in kw else ()):
+                    assert np.array_equal(getattr(fast, k), getattr(slow, k), equal_nan=True), (walker, k)
+        theirs = rm.trace_batch(f, b, d, record_polyline=True, **kw)
+        no_vertex = np.ones(len(f), bool)
+        at_vertex = (theirs.poly_bary == 1.0).any(1)
+        np.logical_and.at(no_vertex, np.repeat(np.arange(len(f)), np.diff(theirs.poly_offsets)), ~at_vertex)
+        assert np.array_equal(fast.face, theirs.face) and np.array_equal(fast.term, theirs.term)
+        assert np.array_equal(fast.q[no_vertex], theirs.q[no_vertex])
+        assert np.abs(fast.q - theirs.q).max() <= 1e-9
+        ok = (fast.status == 0) & (fast.crossings >= 1) & no_vertex
+        Q = fast.q[ok].reshape(-1, 3, 3)
+        n0 = a["fnormal"][f[ok]]
+        # the columns start as the ambient basis (tracer.cpp:60); the first fold drops the start normal and
+        # every fold is an isometry of the tangent planes: Q^T Q = I - n n^T
+        want = np.eye(3)[None] - n0[:, :, None] * n0[:, None, :]
+        assert np.abs(np.einsum("nki,nkj->nij", Q, Q) - want).max() < 1e-9
+
+
+@pytest.mark.parametrize("cache", [True, False])
 def test_hole_avoidance_on_the_fast_walker(gpu, ref, cache):
     """hole_avoidance requests (without polyline / transport matrix) run on the fast walker with
     the full Tracer behind it: boundary edges and boundary vertices -- where hole avoidance acts --
