@@ -278,8 +278,8 @@ def run_ours(args):
             e1.record()
             # the forward results are GFD's base traces (the `trace` argument of gfd_batched, diff.hpp:73)
             mesh.gfd_device(F, B, D, eps, eps, G, jv, jp, grad_v, grad_p, base=o)
-            launches = 1 + 3 + 3  # forward walker + round 1 (job builder, walker on the perp jobs, full walker on the seeds)
-            #                       + round 2 (job builder, walker, assemble); DESIGN.md 3.3
+            launches = 1 + 2 + 3  # forward walker + round 1 (job builder, payload walker on the seeds)
+            #                       + round 2 (job builder, walker on the sibling groups, assemble); DESIGN.md 3.3
         if world > 1:   # results gathered over NVLink; no reduction on this path
             pack[:, 0] = o["face"].double(); pack[:, 1:4] = o["bary"]; pack[:, 4:7] = o["dir"]
             dist.all_gather_into_tensor(gathered, pack)

@@ -1,5 +1,6 @@
 // C-ABI entry points of the differentials and the single-transition operations.
 #include "dg_capi_common.hpp"
+#include <cstdlib>
 
 using namespace dgapi;
 
@@ -16,7 +17,8 @@ int check_common(const dg_mesh* mesh, int64_t n, const char* who) {
 // Runs one batch of trace jobs that already live on the device (GFD rounds).
 cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const double* jb, const double* jd,
                      const double* jp, int32_t* rf, double* rb, double* rd, double* rp, uint8_t* rt, uint8_t* rs,
-                     int max_steps, unsigned long long* total, cudaStream_t stream) {
+                     int max_steps, unsigned long long* total, cudaStream_t stream, int siblings = 0,
+                     int64_t sibling_stride = 0) {
   if (n <= 0) return cudaSuccess;
   dg::TraceParams p{};
   mesh->bind(p);
@@ -25,12 +27,22 @@ cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const do
   p.o_face = rf; p.o_bary = rb; p.o_dir = rd; p.o_payload = rp; p.o_term = rt; p.o_status = rs;
   p.max_steps = max_steps;
   p.refill_min = 0;  // the walker's own default
+  p.siblings = siblings; p.sibling_stride = sibling_stride;
   unsigned long long* ctr = mesh->next_counters();
   p.queue_head = ctr;
   p.total_crossings = total;
   cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   return dg::launch_trace(p, false, jp != nullptr, dg::LaunchShape{mesh->sm_count, 0}, stream);
+}
+
+// DG_GFD_SIBLINGS=0 runs round 2 in plain order (the schedule is a hint: results do not depend on it)
+int gfd_siblings() {
+  static const int k = [] {
+    const char* e = std::getenv("DG_GFD_SIBLINGS");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return k;
 }
 
 }  // namespace
@@ -196,15 +208,39 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   b.degraded = degraded ? st.out(degraded, 4 * N) : st.scratch<uint8_t>(4 * N);
   b.frames = st.out(frames, size_t(DG_FRAME_DOUBLES) * N);
   b.grad_v = st.out(grad_v, 3 * N); b.grad_p = st.out(grad_p, 3 * N);
-  // round 1 / round 2 job and result arrays
-  b.j1_face = st.scratch<int32_t>(4 * N); b.j1_bary = st.scratch<double>(12 * N);
-  b.j1_dir = st.scratch<double>(12 * N); b.j1_payload = st.scratch<double>(12 * N);
-  b.r1_face = st.scratch<int32_t>(4 * N); b.r1_bary = st.scratch<double>(12 * N);
-  b.r1_dir = st.scratch<double>(12 * N); b.r1_payload = st.scratch<double>(12 * N);
-  b.r1_term = st.scratch<uint8_t>(4 * N); b.r1_status = st.scratch<uint8_t>(4 * N);
-  b.j2_face = st.scratch<int32_t>(3 * N); b.j2_bary = st.scratch<double>(9 * N); b.j2_dir = st.scratch<double>(9 * N);
-  b.r2_face = st.scratch<int32_t>(3 * N); b.r2_bary = st.scratch<double>(9 * N);
-  b.r2_term = st.scratch<uint8_t>(3 * N); b.r2_status = st.scratch<uint8_t>(3 * N);
+  // round 1 (seed_u | seed_v) and round 2 (ret_u | ret_v | perp | par or base) job and result arrays
+  b.j1_face = st.scratch<int32_t>(2 * N); b.j1_bary = st.scratch<double>(6 * N);
+  b.j1_dir = st.scratch<double>(6 * N); b.j1_payload = st.scratch<double>(6 * N);
+  b.r1_face = st.scratch<int32_t>(2 * N); b.r1_bary = st.scratch<double>(6 * N);
+  b.r1_dir = nullptr; b.r1_payload = st.scratch<double>(6 * N);   // a seed's end direction is not used, its payload is
+  b.r1_term = st.scratch<uint8_t>(2 * N); b.r1_status = st.scratch<uint8_t>(2 * N);
+  b.j2_face = st.scratch<int32_t>(4 * N); b.j2_bary = st.scratch<double>(12 * N); b.j2_dir = st.scratch<double>(12 * N);
+  b.r2_face = st.scratch<int32_t>(4 * N); b.r2_bary = st.scratch<double>(12 * N);
+  b.r2_term = st.scratch<uint8_t>(4 * N); b.r2_status = st.scratch<uint8_t>(4 * N);
+  double* r2_dir = nullptr;
+  int32_t* par_rface = nullptr; double* par_rbary = nullptr; uint8_t* par_rterm = nullptr; uint8_t* par_rstatus = nullptr;
+  if (known_base) {
+    // the base traces are the caller's forward results (read in place when they are on the device);
+    // the par jobs ride in slots [3n,4n) of round 2
+    b.base_in_round2 = 0;
+    b.base_face = st.in(known_base->face, N); b.base_bary = st.in(known_base->bary, 3 * N);
+    b.base_dir = st.in(known_base->dir, 3 * N);
+    b.base_term = st.in(known_base->term, N); b.base_status = st.in(known_base->status, N);
+    b.par_jface = b.j2_face + 3 * N; b.par_jbary = b.j2_bary + 9 * N; b.par_jdir = b.j2_dir + 9 * N;
+    b.par_face = b.r2_face + 3 * N; b.par_bary = b.r2_bary + 9 * N;
+    b.par_term = b.r2_term + 3 * N; b.par_status = b.r2_status + 3 * N;
+  } else {
+    // the base traces are the fourth sibling of round 2; the par jobs follow in a launch of their own
+    // (job arrays: the seeds' slots [0,n) of round 1, free by then)
+    b.base_in_round2 = 1;
+    r2_dir = st.scratch<double>(12 * N);
+    b.base_face = b.r2_face + 3 * N; b.base_bary = b.r2_bary + 9 * N; b.base_dir = r2_dir ? r2_dir + 9 * N : nullptr;
+    b.base_term = b.r2_term + 3 * N; b.base_status = b.r2_status + 3 * N;
+    b.par_jface = b.j1_face; b.par_jbary = b.j1_bary; b.par_jdir = b.j1_dir;
+    par_rface = st.scratch<int32_t>(N); par_rbary = st.scratch<double>(3 * N);
+    par_rterm = st.scratch<uint8_t>(N); par_rstatus = st.scratch<uint8_t>(N);
+    b.par_face = par_rface; b.par_bary = par_rbary; b.par_term = par_rterm; b.par_status = par_rstatus;
+  }
   b.err = st.scratch<unsigned long long>(8);
   if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_gfd_jacobians staging");
 
@@ -213,30 +249,23 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   h_err[3] = 0;
   st.note(cudaMemcpyAsync(b.err, h_err, sizeof h_err, cudaMemcpyHostToDevice, stream));
 
-  // round 1: base + perp on the lite kernel, the two payload-carrying seeds on the full kernel
+  // round 1: the two payload-carrying eps-length seeds of every sample
   st.note(dg::launch_gfd_round1_jobs(b, stream));
-  if (known_base) {
-    // the base traces are the caller's forward results: only the perp half of the lite jobs runs
-    const cudaMemcpyKind kd = device_mode ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    st.note(cudaMemcpyAsync(b.r1_face, known_base->face, N * sizeof(int32_t), kd, stream));
-    st.note(cudaMemcpyAsync(b.r1_bary, known_base->bary, 3 * N * sizeof(double), kd, stream));
-    st.note(cudaMemcpyAsync(b.r1_dir, known_base->dir, 3 * N * sizeof(double), kd, stream));
-    st.note(cudaMemcpyAsync(b.r1_term, known_base->term, N, kd, stream));
-    st.note(cudaMemcpyAsync(b.r1_status, known_base->status, N, kd, stream));
-    st.note(run_jobs(mesh, n, b.j1_face + N, b.j1_bary + 3 * N, b.j1_dir + 3 * N, nullptr, b.r1_face + N,
-                     b.r1_bary + 3 * N, b.r1_dir + 3 * N, nullptr, b.r1_term + N, b.r1_status + N, max_steps, nullptr,
-                     stream));
-  } else {
-    st.note(run_jobs(mesh, 2 * n, b.j1_face, b.j1_bary, b.j1_dir, nullptr, b.r1_face, b.r1_bary, b.r1_dir, nullptr,
-                     b.r1_term, b.r1_status, max_steps, nullptr, stream));
-  }
-  st.note(run_jobs(mesh, 2 * n, b.j1_face + 2 * N, b.j1_bary + 6 * N, b.j1_dir + 6 * N, b.j1_payload + 6 * N,
-                   b.r1_face + 2 * N, b.r1_bary + 6 * N, b.r1_dir + 6 * N, b.r1_payload + 6 * N, b.r1_term + 2 * N,
-                   b.r1_status + 2 * N, max_steps, nullptr, stream));
-  // round 2: the dependent retraces
+  st.note(run_jobs(mesh, 2 * n, b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, b.r1_face, b.r1_bary, b.r1_dir,
+                   b.r1_payload, b.r1_term, b.r1_status, max_steps, nullptr, stream));
+  // round 2: the full-length jobs of every sample as one sibling group
   st.note(dg::launch_gfd_round2_jobs(b, stream));
-  st.note(run_jobs(mesh, 3 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, nullptr, nullptr,
-                   b.r2_term, b.r2_status, max_steps, nullptr, stream));
+  const int group = gfd_siblings();
+  if (known_base) {
+    st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, nullptr, nullptr,
+                     b.r2_term, b.r2_status, max_steps, nullptr, stream, group ? 3 : 0, n));
+  } else {
+    st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, r2_dir, nullptr,
+                     b.r2_term, b.r2_status, max_steps, nullptr, stream, group ? 4 : 0, n));
+    st.note(dg::launch_gfd_par_jobs(b, stream));
+    st.note(run_jobs(mesh, n, b.par_jface, b.par_jbary, b.par_jdir, nullptr, par_rface, par_rbary, nullptr, nullptr,
+                     par_rterm, par_rstatus, max_steps, nullptr, stream));
+  }
   st.note(dg::launch_gfd_assemble(b, stream));
   st.note(cudaMemcpyAsync(h_err, b.err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
   st.note(cudaStreamSynchronize(stream));
@@ -266,9 +295,9 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   }
   // base end states for callers that chain the forward result
   const cudaMemcpyKind kind = device_mode ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  if (base_face) st.note(cudaMemcpyAsync(base_face, b.r1_face, N * sizeof(int32_t), kind, stream));
-  if (base_bary) st.note(cudaMemcpyAsync(base_bary, b.r1_bary, 3 * N * sizeof(double), kind, stream));
-  if (base_dir) st.note(cudaMemcpyAsync(base_dir, b.r1_dir, 3 * N * sizeof(double), kind, stream));
+  if (base_face) st.note(cudaMemcpyAsync(base_face, b.base_face, N * sizeof(int32_t), kind, stream));
+  if (base_bary) st.note(cudaMemcpyAsync(base_bary, b.base_bary, 3 * N * sizeof(double), kind, stream));
+  if (base_dir) st.note(cudaMemcpyAsync(base_dir, b.base_dir, 3 * N * sizeof(double), kind, stream));
   cudaError_t e = st.finish();
   if (e != cudaSuccess) return fail_cuda(e, "dg_gfd_jacobians");
 

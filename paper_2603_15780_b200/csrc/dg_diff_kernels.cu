@@ -7,8 +7,15 @@
 //
 // GFD job layout (ours, not the reference's interleaved 4i+k): the jobs of one kind are
 // contiguous so that each round is ONE launch per kernel variant --
-//   round 1: [0,n) base  [n,2n) perp  | [2n,3n) seed_u  [3n,4n) seed_v   (lite | payload)
-//   round 2: [0,n) par   [n,2n) ret_u   [2n,3n) ret_v                      (lite)
+//   round 1: [0,n) seed_u  [n,2n) seed_v                                  (payload kernel, eps-length)
+//   round 2: [0,n) ret_u  [n,2n) ret_v  [2n,3n) perp  [3n,4n) par | base  (lite)
+// The full-length jobs of a sample (ret_u, ret_v, perp -- and its base trace when the caller does
+// not bring one) differ by an O(eps) offset and cross the same faces: round 2 runs them as a
+// sibling group in one warp (TraceParams::siblings, stride n) so that they share every
+// crossing-record fetch. With the caller's forward results as base traces the group has three
+// members and the eps-length par jobs fill the tail of the same launch; without, the base trace is
+// the fourth member and the par jobs (which start where the base ends) get a short launch of
+// their own.
 //   fallback rounds (only if some + perturbation left the mesh):
 //   round 3: [0,n) par-  [n,2n) perp-   [2n,3n) back_u  [3n,4n) back_v    (payload)
 //   round 4: [0,n) retrace of back_u    [n,2n) retrace of back_v          (lite)
@@ -164,14 +171,16 @@ __global__ void __launch_bounds__(128) gfd_round1_jobs_kernel(const __grid_const
   const bool face_ok = f >= 0 && f < b.mesh.nf;
   if (!face_ok || !make_tangent_frame(b.mesh, f, v, &fv)) {  // diff.cpp:284 throws for the whole call
     note_error(b.err + 0, i);
-    for (int k = 0; k < 4; ++k) put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, k * n + i, f, p, zero, zero);
+    for (int k = 0; k < 2; ++k) put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, k * n + i, f, p, zero, zero);
+    put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, 2 * n + i, f, p, zero, zero);
+    if (b.base_in_round2) put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, 3 * n + i, f, p, zero, zero);
     return;
   }
   const BaryFrame fp = make_bary_frame(load_face<double>(b.mesh, f));
-  put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, i, f, p, v, zero);                             // base
-  put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, n + i, f, p, v + fv.e_perp * b.eps_v, zero);   // perp
-  put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, 2 * n + i, f, p, fp.u_hat * b.eps_p, v);       // seed_u
-  put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, 3 * n + i, f, p, fp.v_hat * b.eps_p, v);       // seed_v
+  put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, i, f, p, fp.u_hat * b.eps_p, v);              // seed_u
+  put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, n + i, f, p, fp.v_hat * b.eps_p, v);          // seed_v
+  put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, 2 * n + i, f, p, v + fv.e_perp * b.eps_v, zero);   // perp (runs in round 2)
+  if (b.base_in_round2) put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, 3 * n + i, f, p, v, zero);   // base (ditto)
   if (b.frames) store_frames(b.frames, i, &fv, &fp, nullptr);
 }
 
@@ -182,21 +191,35 @@ __global__ void __launch_bounds__(128) gfd_round2_jobs_kernel(const __grid_const
   const V zero{0.0, 0.0, 0.0};
   const V p = ld3(b.bary, i);
   const int f = b.face[i];
-  // require_base, diff.cpp:121-124
-  if (!reached(b.r1_status[i], b.r1_term[i])) {
-    note_error(b.err + 1, i);
-    for (int k = 0; k < 3; ++k) put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, k * n + i, f, p, zero, zero);
-    return;
+  if (!b.base_in_round2) {
+    // require_base, diff.cpp:121-124
+    if (!reached(b.base_status[i], b.base_term[i])) {
+      note_error(b.err + 1, i);
+      for (int k = 0; k < 4; ++k) put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, k * n + i, f, p, zero, zero);
+      return;
+    }
+    put_job(b.par_jface, b.par_jbary, b.par_jdir, nullptr, i, b.base_face[i], ld3(b.base_bary, i), ld3(b.base_dir, i) * b.eps_v, zero);
   }
-  put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, i, b.r1_face[i], ld3(b.r1_bary, i), ld3(b.r1_dir, i) * b.eps_v, zero);
-  for (int k = 2; k <= 3; ++k) {  // diff.cpp:302-308
+  for (int k = 0; k < 2; ++k) {  // diff.cpp:302-308: ret_u, ret_v from the seeds' end states
     const int64_t s = k * n + i;
     if (reached(b.r1_status[s], b.r1_term[s]))
-      put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, (k - 1) * n + i, b.r1_face[s], ld3(b.r1_bary, s),
-              ld3(b.r1_payload, s), zero);
+      put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, s, b.r1_face[s], ld3(b.r1_bary, s), ld3(b.r1_payload, s), zero);
     else
-      put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, (k - 1) * n + i, f, p, zero, zero);
+      put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, s, f, p, zero, zero);
   }
+}
+
+// Without a caller-provided base: the par jobs start where the base traces of round 2 ended.
+__global__ void __launch_bounds__(128) gfd_par_jobs_kernel(const __grid_constant__ GfdBuffers b) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= b.n) return;
+  const V zero{0.0, 0.0, 0.0};
+  if (!reached(b.base_status[i], b.base_term[i])) {  // require_base, diff.cpp:121-124
+    note_error(b.err + 1, i);
+    put_job(b.par_jface, b.par_jbary, b.par_jdir, nullptr, i, b.face[i], ld3(b.bary, i), zero, zero);
+    return;
+  }
+  put_job(b.par_jface, b.par_jbary, b.par_jdir, nullptr, i, b.base_face[i], ld3(b.base_bary, i), ld3(b.base_dir, i) * b.eps_v, zero);
 }
 
 // Endpoint of a finished job in ambient space.
@@ -221,13 +244,13 @@ __global__ void __launch_bounds__(128) gfd_assemble_kernel(const __grid_constant
   TangentFrame fv;
   make_tangent_frame(b.mesh, f, v, &fv);
   const BaryFrame fp = make_bary_frame(load_face<double>(b.mesh, f));
-  const Face<double> cb = load_face<double>(b.mesh, b.r1_face[i]);
+  const Face<double> cb = load_face<double>(b.mesh, b.base_face[i]);
   const BaryFrame fo = make_bary_frame(cb);
-  const V ref = embed(cb, ld3(b.r1_bary, i));
+  const V ref = embed(cb, ld3(b.base_bary, i));
   if (kPhase == 0 && b.frames) store_frames(b.frames, i, nullptr, nullptr, &fo);
 
   // seeds must have traced, diff.cpp:182-184
-  if (!reached(b.r1_status[2 * n + i], b.r1_term[2 * n + i]) || !reached(b.r1_status[3 * n + i], b.r1_term[3 * n + i])) {
+  if (!reached(b.r1_status[i], b.r1_term[i]) || !reached(b.r1_status[n + i], b.r1_term[n + i])) {
     note_error(b.err + 2, i);
     return;
   }
@@ -235,11 +258,12 @@ __global__ void __launch_bounds__(128) gfd_assemble_kernel(const __grid_constant
   V col[4];  // par, perp, u, v
   bool deg[4] = {false, false, false, false};
   {  // + side (fd_column :130-137)
-    const int64_t slot[4] = {i, n + i, n + i, 2 * n + i};
-    const uint8_t* st[4] = {b.r2_status, b.r1_status, b.r2_status, b.r2_status};
-    const uint8_t* tm[4] = {b.r2_term, b.r1_term, b.r2_term, b.r2_term};
-    const int32_t* rf[4] = {b.r2_face, b.r1_face, b.r2_face, b.r2_face};
-    const double* rb[4] = {b.r2_bary, b.r1_bary, b.r2_bary, b.r2_bary};
+    // par (its own result arrays, indexed by sample), perp, u, v (round 2)
+    const int64_t slot[4] = {i, 2 * n + i, i, n + i};
+    const uint8_t* st[4] = {b.par_status, b.r2_status, b.r2_status, b.r2_status};
+    const uint8_t* tm[4] = {b.par_term, b.r2_term, b.r2_term, b.r2_term};
+    const int32_t* rf[4] = {b.par_face, b.r2_face, b.r2_face, b.r2_face};
+    const double* rb[4] = {b.par_bary, b.r2_bary, b.r2_bary, b.r2_bary};
     const double eps[4] = {b.eps_v, b.eps_v, b.eps_p, b.eps_p};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -305,7 +329,7 @@ __global__ void __launch_bounds__(128) gfd_fallback_jobs_kernel(const __grid_con
   make_tangent_frame(b.mesh, f, v, &fv);
   const BaryFrame fp = make_bary_frame(load_face<double>(b.mesh, f));
   if (dflag[0])  // diff.cpp:161
-    put_job(b.j3_face, b.j3_bary, b.j3_dir, b.j3_payload, i, b.r1_face[i], ld3(b.r1_bary, i), ld3(b.r1_dir, i) * -b.eps_v, zero);
+    put_job(b.j3_face, b.j3_bary, b.j3_dir, b.j3_payload, i, b.base_face[i], ld3(b.base_bary, i), ld3(b.base_dir, i) * -b.eps_v, zero);
   if (dflag[1])  // diff.cpp:167
     put_job(b.j3_face, b.j3_bary, b.j3_dir, b.j3_payload, n + i, f, p, v - fv.e_perp * b.eps_v, zero);
   if (dflag[2])  // diff.cpp:187-190
@@ -453,6 +477,10 @@ cudaError_t launch_gfd_round1_jobs(const GfdBuffers& b, cudaStream_t stream) {
 }
 cudaError_t launch_gfd_round2_jobs(const GfdBuffers& b, cudaStream_t stream) {
   gfd_round2_jobs_kernel<<<grid_for(b.n, 128), 128, 0, stream>>>(b);
+  return cudaGetLastError();
+}
+cudaError_t launch_gfd_par_jobs(const GfdBuffers& b, cudaStream_t stream) {
+  gfd_par_jobs_kernel<<<grid_for(b.n, 128), 128, 0, stream>>>(b);
   return cudaGetLastError();
 }
 cudaError_t launch_gfd_assemble(const GfdBuffers& b, cudaStream_t stream) {

@@ -42,6 +42,12 @@ struct TraceParams {
   unsigned long long* total_crossings;  // optional: += sum of crossings of the batch
   int32_t max_steps;
   int32_t refill_min;  // refill a warp once this many lanes are idle (0 = the walker's default)
+  // Sibling schedule (perm must be null): the first siblings * sibling_stride elements of the schedule are
+  // groups of `siblings` queries {g, g + stride, ..., g + (siblings-1) stride}, handed to lanes of ONE warp
+  // together. GFD's re-traces of one sample follow the same faces step for step, so the group gathers the
+  // same crossing records at the same time: one HBM / L2 line serves all of them. 0 / 1 = plain order.
+  int32_t siblings;
+  int64_t sibling_stride;
   uint8_t hole_avoidance;
   uint8_t want_q;
   uint8_t he_map_ok;  // he_map is a valid tensor map of mesh.he
@@ -88,13 +94,21 @@ struct GfdBuffers {
   const double* bary;
   const double* v;
   double eps_v, eps_p;
-  // round-1 job arrays (4n) and results
+  // round-1 job arrays (2n: seed_u | seed_v) and results
   int32_t* j1_face; double* j1_bary; double* j1_dir; double* j1_payload;
   int32_t* r1_face; double* r1_bary; double* r1_dir; double* r1_payload;
   uint8_t* r1_term; uint8_t* r1_status;
-  // round-2 job arrays (3n) and results
+  // round-2 job arrays (4n: ret_u | ret_v | perp | par or base) and results
   int32_t* j2_face; double* j2_bary; double* j2_dir;
   int32_t* r2_face; double* r2_bary; uint8_t* r2_term; uint8_t* r2_status;
+  // the base traces, indexed by sample: the caller's forward results, or slots [3n,4n) of round 2
+  const int32_t* base_face; const double* base_bary; const double* base_dir;
+  const uint8_t* base_term; const uint8_t* base_status;
+  uint8_t base_in_round2;
+  // the par jobs and their results, indexed by sample: slots [3n,4n) of round 2 with a known base,
+  // arrays of their own otherwise
+  int32_t* par_jface; double* par_jbary; double* par_jdir;
+  const int32_t* par_face; const double* par_bary; const uint8_t* par_term; const uint8_t* par_status;
   // fallback rounds (4n slots, only flagged columns are live)
   int32_t* j3_face; double* j3_bary; double* j3_dir; double* j3_payload;
   int32_t* r3_face; double* r3_bary; double* r3_payload; uint8_t* r3_term; uint8_t* r3_status;
@@ -110,6 +124,7 @@ struct GfdBuffers {
 };
 cudaError_t launch_gfd_round1_jobs(const GfdBuffers& b, cudaStream_t stream);
 cudaError_t launch_gfd_round2_jobs(const GfdBuffers& b, cudaStream_t stream);
+cudaError_t launch_gfd_par_jobs(const GfdBuffers& b, cudaStream_t stream);
 cudaError_t launch_gfd_assemble(const GfdBuffers& b, cudaStream_t stream);
 cudaError_t launch_gfd_fallback_jobs(const GfdBuffers& b, cudaStream_t stream);
 cudaError_t launch_gfd_fallback_round2_jobs(const GfdBuffers& b, cudaStream_t stream);

@@ -194,13 +194,17 @@ bool fast_walk_enabled() {
 
 // The crossing records are gathered with 256-bit loads while they fit the load path's TLB reach
 // and with one TMA bulk copy per record beyond (DG_FAST_TMA=0|1 forces either; dg_fast_walk.cuh).
-bool tma_gather(const MeshView& m) {
+// A sibling schedule (TraceParams::siblings, GFD round 2) keeps the loads at every size: the lanes of a
+// group ask for the same line, the load path merges them into one request and one TLB lookup, and three
+// re-traces cost less than one lone trace (7.8 M faces / 3 GB of records: 40 ms against 50 ms with TMA,
+// profiles/tuning_r1.md); the TMA engine fetches every row of a gather4 on its own.
+bool tma_gather(const MeshView& m, int siblings = 0) {
   static const int forced = [] {
     const char* e = getenv("DG_FAST_TMA");
     return e ? (!strcmp(e, "0") || !strcmp(e, "off") ? 0 : 1) : -1;
   }();
   if (forced >= 0) return forced != 0;
-  return size_t(m.nf) * 3 * sizeof(HalfEdgeRec) > (size_t(250) << 20);
+  return siblings <= 1 && size_t(m.nf) * 3 * sizeof(HalfEdgeRec) > (size_t(250) << 20);
 }
 
 }  // namespace
@@ -213,7 +217,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
-  const bool tma = p.mesh.he && p.he_map_ok && (shape.walker == 3 || (shape.walker != 2 && tma_gather(p.mesh)));
+  const bool tma = p.mesh.he && p.he_map_ok && (shape.walker == 3 || (shape.walker != 2 && tma_gather(p.mesh, p.siblings)));
   if (!needs_full && shape.walker != 1 && fast_walk_enabled()) {
     if (!p.mesh.he) return launch_fast<false, false>(p, shape, stream);
     return tma ? launch_fast<true, true>(p, shape, stream) : launch_fast<true, false>(p, shape, stream);

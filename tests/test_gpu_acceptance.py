@@ -59,11 +59,14 @@ def test_criterion_5_gfd_over_ep_cost_ratio(gpu, ref):
     f, b, v = rm.sample_queries(45, 200000, 0.1, np.pi / 2)
     g = np.random.default_rng(0).normal(size=(len(f), 3))
 
-    def timed(fn):
+    def timed(fn):   # best of 3 after a warm-up call: wall clock of host-mode calls (staging pools, pageable copies)
         fn()
-        t0 = time.perf_counter()
-        fn()
-        return time.perf_counter() - t0
+        best = np.inf
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fn()
+            best = min(best, time.perf_counter() - t0)
+        return best
 
     def ep():
         t = m.trace_batch(f, b, v)
