@@ -388,6 +388,11 @@ def run_ours(args):
                 "geodesics_per_s": geodesics_per_s,
                 "forward_only": {"ms": float(np.mean(tr_ms)), "face_crossings_per_s": crossings_per_step / t_trace,
                                  "geodesics_per_s": n / t_trace},
+                # rank 0's own step minus its forward trace; GFD re-traces every sample three times at full length
+                # (sibling groups), so its rate counts 3 x the forward crossings
+                "backward_only": {"scheme": scheme, "ms": float(np.mean(step_ms) - np.mean(tr_ms)),
+                                  "retraced_face_crossings_per_s": (3 * crossings_per_step / ((np.mean(step_ms) - np.mean(tr_ms)) * 1e-3)
+                                                                    if scheme == "gfd" else None)},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
                              "kernel": ("trace_fast_kernel<crossing records, TMA tile::gather4>" if mesh.uses_tma_gather else
