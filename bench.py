@@ -160,15 +160,21 @@ def cpu_reference(xyz, tri, f, b, d, q, scheme, budget_s=12.0, reps=3):
     if not refapi.available():
         raise RuntimeError("oracle/_ref/libdigeo_ref.so missing")
     rm = refapi.RefMesh.build(xyz, tri)
-    threads = refapi.resolve_workers(0)
+    # all host threads this process may run on, passed explicitly: torchrun exports OMP_NUM_THREADS=1, which the
+    # reference's workers <= 0 default (tracer.cpp:547-555) would follow
+    try:
+        threads = len(os.sched_getaffinity(0))
+    except AttributeError:
+        threads = os.cpu_count() or 1
+    threads = refapi.resolve_workers(threads)
 
     def run(k):
         t0 = time.perf_counter()
-        r = rm.trace_batch(f[:k], b[:k], d[:k], workers=0)
+        r = rm.trace_batch(f[:k], b[:k], d[:k], workers=threads)
         if scheme == "ep":   # ep_jacobians + pullback_ambient per sample, the reference's serial loop
             rm.ep(f[:k], b[:k], d[:k], r.face, r.bary, r.dir, g=q[:k])
         else:
-            rm.gfd(f[:k], b[:k], d[:k], g=q[:k], workers=0)
+            rm.gfd(f[:k], b[:k], d[:k], g=q[:k], workers=threads)
         return time.perf_counter() - t0
 
     k = min(len(f), 2000)
@@ -177,7 +183,7 @@ def cpu_reference(xyz, tri, f, b, d, q, scheme, budget_s=12.0, reps=3):
     times = [run(k) for _ in range(reps)]
     best = float(np.median(times))
     # crossings of the sample, counted from the reference's own polylines
-    cnt = rm.trace_batch(f[:k], b[:k], d[:k], record_polyline=True, workers=0)
+    cnt = rm.trace_batch(f[:k], b[:k], d[:k], record_polyline=True, workers=threads)
     crossings = int((cnt.npoints - 2).clip(min=0).sum())
     return crossings / best, k / best, f"first {k} of {len(f)} geodesics, median of {reps}", threads, best * 1e3, crossings, k
 
