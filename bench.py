@@ -384,7 +384,7 @@ def run_ours(args):
         alg_bytes = crossings_per_step * BYTES_PER_CROSSING + n * BYTES_PER_GEODESIC
         achieved = alg_bytes / t_trace / 1e9
         traffic = profile_traffic(args.workload)
-        info = dg.kernel_info(False, False, cached=mesh.has_transport_cache, tma=mesh.uses_tma_gather)
+        info = dg.kernel_info(False, False, cached=mesh.has_transport_cache, tma=mesh.gather == "tma", coop=mesh.gather == "coop")
         line = {"metric": f"face_crossings_per_s_fwd_{scheme}", "value": value, "unit": "face-crossings/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -401,7 +401,8 @@ def run_ours(args):
                                                                     if scheme == "gfd" else None)},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
-                             "kernel": ("trace_fast_kernel<crossing records, TMA tile::gather4>" if mesh.uses_tma_gather else
+                             "kernel": ("trace_fast_kernel<crossing records, TMA tile::gather4>" if mesh.gather == "tma" else
+                                        "trace_fast_kernel<crossing records, cooperative 256-bit loads>" if mesh.gather == "coop" else
                                         "trace_fast_kernel<crossing records, 256-bit loads>" if mesh.has_transport_cache else
                                         "trace_fast_kernel<face records>"),
                              "peak_source": peak_src,

@@ -72,7 +72,7 @@ enum { DG_EVENT_ADVANCED = 0, DG_EVENT_CROSSED_EDGE = 1, DG_EVENT_CROSSED_VERTEX
        DG_EVENT_BOUNDARY_SLIDE = 3, DG_EVENT_BOUNDARY_STOP = 4 };
 
 enum { DG_MEM_HOST = 0, DG_MEM_DEVICE = 1 };
-enum { DG_WALKER_AUTO = 0, DG_WALKER_GENERIC = 1, DG_WALKER_FAST_LOADS = 2, DG_WALKER_FAST_TMA = 3 };
+enum { DG_WALKER_AUTO = 0, DG_WALKER_GENERIC = 1, DG_WALKER_FAST_LOADS = 2, DG_WALKER_FAST_TMA = 3, DG_WALKER_FAST_COOP = 4 };
 /* Arithmetic of the f64 tracer: there is ONE lane. The library is built without FMA contraction
  * and follows the reference's operation order, so a trace that never takes a vertex branch (no
  * libm calls) is bit-identical to the reference CPU build; vertex branches agree to the last
@@ -109,17 +109,21 @@ DG_API int dg_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int
  * half-edge: the fold isometry of tracer.cpp:113-126 plus the two corner-0 edge vectors of the
  * entered face (computed on the device at upload by the same code the uncached walker runs, so
  * results are bit-identical). AUTO enables it while the records stay within 16 GB (about 40 M
- * faces): the fast walker gathers them with 256-bit loads up to 250 MB and through TMA
- * tile::gather4 beyond (the load path falls off its TLB reach there). Env
- * DG_TRANSPORT_CACHE=on|off overrides AUTO. */
+ * faces): the fast walker gathers them with four 256-bit loads per lane up to 250 MB and with
+ * cooperative 256-bit loads (four lanes per record, one request per line) beyond, where the
+ * per-lane loads fall off a cliff; TMA tile::gather4 is the third, selectable gather
+ * (dg_trace_cfg.walker). Env DG_TRANSPORT_CACHE=on|off overrides AUTO. */
 enum { DG_MESH_TRANSPORT_AUTO = 0, DG_MESH_TRANSPORT_ON = 1, DG_MESH_TRANSPORT_OFF = 2 };
 DG_API int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf,
                              const int32_t* adj, const double* fnormal, const double* vangle,
                              const uint8_t* vboundary, const int32_t* csr_off,
                              const int32_t* csr_list, uint32_t flags, dg_mesh** out);
 DG_API int dg_mesh_has_transport_cache(const dg_mesh* m);
-/* 1 when the fast walker fetches this mesh's crossing records through TMA tile::gather4 (records
- * beyond 250 MB), 0 when it gathers them with 256-bit loads or the mesh has none. */
+/* How the fast walker gathers this mesh's crossing records for a batch of lone traces
+ * (DG_WALKER_AUTO): per-lane 256-bit loads (also: no records), TMA tile::gather4, or cooperative
+ * 256-bit loads. dg_mesh_uses_tma_gather: 1 iff that is DG_GATHER_TMA. */
+enum { DG_GATHER_LOADS = 0, DG_GATHER_TMA = 1, DG_GATHER_COOP = 2 };
+DG_API int dg_mesh_gather_mode(const dg_mesh* m);
 DG_API int dg_mesh_uses_tma_gather(const dg_mesh* m);
 DG_API void dg_mesh_destroy(dg_mesh* m);
 DG_API int32_t dg_mesh_face_count(const dg_mesh* m);
@@ -141,10 +145,10 @@ typedef struct dg_trace_cfg {
                                     4 with a bounded wait for the fast walker, 1 for the general one) */
   uint8_t blocks_per_sm;         /* resident CTAs per SM of the persistent grid (0 = occupancy query) */
   uint8_t walker;                /* DG_WALKER_AUTO: the fast walker whenever the request is the plain f64
-                                    forward map, gathering the crossing records with 256-bit loads up to
-                                    250 MB of records and through TMA tile::gather4 beyond;
+                                    forward map, gathering the crossing records with per-lane 256-bit loads
+                                    up to 250 MB of records and with cooperative loads beyond;
                                     DG_WALKER_GENERIC: always the general state machine; DG_WALKER_FAST_LOADS /
-                                    DG_WALKER_FAST_TMA: the fast walker with that gather. Same bits whatever
+                                    DG_WALKER_FAST_TMA / DG_WALKER_FAST_COOP: the fast walker with that gather. Same bits whatever
                                     the choice; selectable for cross-checks and measurements */
   uint8_t reserved[3];
   void* stream;                  /* cudaStream_t to launch on. DG_MEM_HOST: NULL = the mesh's private
@@ -187,7 +191,7 @@ DG_API int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in,
                           const dg_trace_cfg* cfg, dg_trace_out* out);
 
 /* Registers per thread, resident CTAs per SM and CTA size of a tracer kernel variant.
- * full: bit 2 = the TMA-gather variant of the fast walker,
+ * full: bit 2 = the TMA-gather variant of the fast walker, bit 3 = its cooperative-loads variant,
  *       bit 0 = payload / transport matrix / hole avoidance / polyline support compiled in,
  *       bit 1 = transport-cache variant. */
 DG_API void dg_trace_kernel_info(int use_f32, int full, int* regs, int* blocks_per_sm,

@@ -64,6 +64,7 @@ class Mesh:
         self.transport_cache = transport_cache
         self.has_transport_cache = False
         self.uses_tma_gather = False
+        self.gather = "loads"      # how lone traces fetch the crossing records: loads | tma | coop
         self.xyz = _f64(xyz).reshape(-1, 3)
         self.tri = _i32(tri).reshape(-1, 3)
         nv, nf = len(self.xyz), len(self.tri)
@@ -102,6 +103,7 @@ class Mesh:
         self.h = h
         self.has_transport_cache = bool(L.dg_mesh_has_transport_cache(h))
         self.uses_tma_gather = bool(L.dg_mesh_uses_tma_gather(h))
+        self.gather = ("loads", "tma", "coop")[L.dg_mesh_gather_mode(h)]
         return self
 
     def __del__(self):
@@ -312,7 +314,7 @@ class Mesh:
 
 
 # dg_trace_cfg.walker (DG_WALKER_*): which kernel traces a plain f64 forward request
-WALKERS = {"auto": 0, "generic": 1, "loads": 2, "tma": 3}
+WALKERS = {"auto": 0, "generic": 1, "loads": 2, "tma": 3, "coop": 4}
 
 
 class Batch:
@@ -384,8 +386,8 @@ class Batch:
         return out
 
 
-def kernel_info(use_f32=False, full=False, cached=False, tma=False):
+def kernel_info(use_f32=False, full=False, cached=False, tma=False, coop=False):
     regs, bps, bt = C.c_int(0), C.c_int(0), C.c_int(0)
-    lib().dg_trace_kernel_info(int(use_f32), int(full) | (int(cached) << 1) | (int(tma) << 2), C.addressof(regs), C.addressof(bps),
+    lib().dg_trace_kernel_info(int(use_f32), int(full) | (int(cached) << 1) | (int(tma) << 2) | (int(coop) << 3), C.addressof(regs), C.addressof(bps),
                                C.addressof(bt))
     return dict(registers=regs.value, blocks_per_sm=bps.value, block_threads=bt.value)

@@ -373,7 +373,8 @@ void dg_mesh_destroy(dg_mesh* m) {
 }
 
 int dg_mesh_has_transport_cache(const dg_mesh* m) { return m && m->he ? 1 : 0; }
-int dg_mesh_uses_tma_gather(const dg_mesh* m) { return m && dg::fast_walker_uses_tma(m->view(), m->he_map_ok) ? 1 : 0; }
+int dg_mesh_gather_mode(const dg_mesh* m) { return m ? dg::fast_walker_gather_mode(m->view(), m->he_map_ok) : 0; }
+int dg_mesh_uses_tma_gather(const dg_mesh* m) { return dg_mesh_gather_mode(m) == DG_GATHER_TMA ? 1 : 0; }
 int32_t dg_mesh_face_count(const dg_mesh* m) { return m ? m->nf : 0; }
 int32_t dg_mesh_vertex_count(const dg_mesh* m) { return m ? m->nv : 0; }
 int64_t dg_mesh_device_bytes(const dg_mesh* m) { return m ? m->bytes : 0; }

@@ -64,7 +64,8 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
                          cudaStream_t stream);
 
 // Whether the fast walker gathers this mesh's crossing records through TMA (AUTO policy).
-bool fast_walker_uses_tma(const MeshView& m, bool map_ok);
+// gather of the crossing records for a lone-trace batch on this mesh: 0 per-lane loads, 1 TMA, 2 cooperative loads
+int fast_walker_gather_mode(const MeshView& m, bool map_ok);
 
 // Kernel attributes for reporting (registers, max resident blocks per SM).
 void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads);

@@ -8,6 +8,7 @@
 // query in place. The grid is sized to the resident capacity of the chip (SM count x
 // resident blocks per SM), never to the batch.
 #include <atomic>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -157,7 +158,7 @@ cudaError_t launch_one(const TraceParams& p_in, LaunchShape shape, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <bool kCached, bool kTma, int kPay = 0>
+template <bool kCached, int kTma, int kPay = 0>
 cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t stream) {
   constexpr size_t smem = kTma ? size_t(kFastTmaSmemBytes) : 0;
   TraceParams p = p_in;
@@ -192,24 +193,36 @@ bool fast_walk_enabled() {
   return on;
 }
 
-// The crossing records are gathered with 256-bit loads while they fit the load path's TLB reach
-// and with one TMA bulk copy per record beyond (DG_FAST_TMA=0|1 forces either; dg_fast_walk.cuh).
-// A sibling schedule (TraceParams::siblings, GFD round 2) keeps the loads at every size: the lanes of a
-// group ask for the same line, the load path merges them into one request and one TLB lookup, and three
-// re-traces cost less than one lone trace (7.8 M faces / 3 GB of records: 40 ms against 50 ms with TMA,
-// profiles/tuning_r1.md); the TMA engine fetches every row of a gather4 on its own.
-bool tma_gather(const MeshView& m, int siblings = 0) {
+// How the fast walker gathers the crossing records (dg_fast_walk.cuh): 0 = four 256-bit loads per lane,
+// 1 = TMA tile::gather4, 2 = cooperative 256-bit loads (four lanes per record, sectors handed to their owner
+// through shared memory). Measured (profiles/tuning_r1.md; scripts/micro/gather_bench.cu):
+//  * lone traces, records within 250 MB (c2): per-lane loads -- 3.80 ms against 4.01 (cooperative) and 4.37 (TMA):
+//    the walker is issue-bound there and the per-lane loads cost the fewest instructions;
+//  * lone traces beyond (c3 and up): per-lane loads fall off a cliff (one request and one address translation per
+//    sector: 37 ms on c3); cooperative loads send one request per record like TMA and need no barrier wait:
+//    c3 18.2 ms against 19.4 (TMA), 2.25 M faces 9.7 / 10.3, 7.8 M faces 19.4 / 19.8, config-4 batch 14.6 / 15.7;
+//  * a sibling schedule (TraceParams::siblings, GFD round 2): per-lane loads at every size -- the lanes of a group ask
+//    for the same line and the load path merges them (c3: 45.3 ms against 52.8 cooperative, 55.9 TMA).
+// DG_FAST_GATHER=loads|tma|coop forces one (A/B measurements); dg_trace_cfg.walker selects one per call.
+int gather_mode(const MeshView& m, int siblings, bool map_ok, int walker) {
+  if (!m.he) return 0;
   static const int forced = [] {
-    const char* e = getenv("DG_FAST_TMA");
-    return e ? (!strcmp(e, "0") || !strcmp(e, "off") ? 0 : 1) : -1;
+    const char* e = getenv("DG_FAST_GATHER");
+    return !e ? -1 : !strcmp(e, "loads") ? 0 : !strcmp(e, "tma") ? 1 : !strcmp(e, "coop") ? 2 : -1;
   }();
-  if (forced >= 0) return forced != 0;
-  return siblings <= 1 && size_t(m.nf) * 3 * sizeof(HalfEdgeRec) > (size_t(250) << 20);
+  int mode;
+  if (walker == 2) mode = 0;
+  else if (walker == 3) mode = 1;
+  else if (walker == 4) mode = 2;
+  else if (forced >= 0) mode = forced;
+  else mode = (siblings <= 1 && size_t(m.nf) * 3 * sizeof(HalfEdgeRec) > (size_t(250) << 20)) ? 2 : 0;
+  if (mode == 1 && !map_ok) mode = 2;
+  return mode;
 }
 
 }  // namespace
 
-bool fast_walker_uses_tma(const MeshView& m, bool map_ok) { return m.he && map_ok && fast_walk_enabled() && tma_gather(m); }
+int fast_walker_gather_mode(const MeshView& m, bool map_ok) { return fast_walk_enabled() ? gather_mode(m, 0, map_ok, 0) : 0; }
 
 cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
                          cudaStream_t stream) {
@@ -217,24 +230,22 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
-  const bool tma = p.mesh.he && p.he_map_ok && (shape.walker == 3 || (shape.walker != 2 && tma_gather(p.mesh, p.siblings)));
-  if (!needs_full && shape.walker != 1 && fast_walk_enabled()) {
-    if (!p.mesh.he) return launch_fast<false, false>(p, shape, stream);
-    return tma ? launch_fast<true, true>(p, shape, stream) : launch_fast<true, false>(p, shape, stream);
-  }
+  const int gather = gather_mode(p.mesh, p.siblings, p.he_map_ok != 0, shape.walker);
+  auto fast = [&](auto pay) {
+    constexpr int kPay = decltype(pay)::value;
+    if (!p.mesh.he) return launch_fast<false, 0, kPay>(p, shape, stream);
+    return gather == 1 ? launch_fast<true, 1, kPay>(p, shape, stream)
+         : gather == 2 ? launch_fast<true, 2, kPay>(p, shape, stream)
+                       : launch_fast<true, 0, kPay>(p, shape, stream);
+  };
+  if (!needs_full && shape.walker != 1 && fast_walk_enabled()) return fast(std::integral_constant<int, 0>{});
   // a payload to transport, hole avoidance, a polyline to record -- anything but the transport matrix:
   // the fast walker carries the payload along, writes one polyline point per step and leaves boundary
   // events to the full Tracer behind it
   const bool payload_only = (p.payload || p.o_payload || p.hole_avoidance || p.poly_offsets) && !p.want_q && !p.o_transport;
-  if (payload_only && shape.walker != 1 && fast_walk_enabled()) {
-    if (!p.mesh.he) return launch_fast<false, false, 1>(p, shape, stream);
-    return tma ? launch_fast<true, true, 1>(p, shape, stream) : launch_fast<true, false, 1>(p, shape, stream);
-  }
+  if (payload_only && shape.walker != 1 && fast_walk_enabled()) return fast(std::integral_constant<int, 1>{});
   // the transport matrix as well: three more vectors through every fold isometry
-  if (p.want_q && shape.walker != 1 && fast_walk_enabled()) {
-    if (!p.mesh.he) return launch_fast<false, false, 2>(p, shape, stream);
-    return tma ? launch_fast<true, true, 2>(p, shape, stream) : launch_fast<true, false, 2>(p, shape, stream);
-  }
+  if (p.want_q && shape.walker != 1 && fast_walk_enabled()) return fast(std::integral_constant<int, 2>{});
   if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
   return needs_full ? launch_one<double, true, false>(p, shape, stream) : launch_one<double, false, false>(p, shape, stream);
 }
@@ -242,7 +253,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
 void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads) {
   cudaFuncAttributes a{};
   int per_sm = 0, threads = kBlockThreads;
-  const bool full = variant & 1, cached = (variant & 2) && !use_f32, tma = (variant & 4) != 0;
+  const bool full = variant & 1, cached = (variant & 2) && !use_f32, tma = (variant & 4) != 0, coop = (variant & 8) != 0;
   auto query = [&](auto kernel, int block) {
     cudaFuncGetAttributes(&a, kernel);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
@@ -252,13 +263,17 @@ void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm,
     if (full) query(trace_kernel<float, true, false>, kBlockThreads); else query(trace_kernel<float, false, false>, kBlockThreads);
   } else if (!full && fast_walk_enabled()) {
     if (cached && tma) {
-      cudaFuncGetAttributes(&a, trace_fast_kernel<true, true>);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<true, true>, DG_FAST_BLOCK, kFastTmaSmemBytes);
+      cudaFuncGetAttributes(&a, trace_fast_kernel<true, 1>);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<true, 1>, DG_FAST_BLOCK, kFastTmaSmemBytes);
+      threads = DG_FAST_BLOCK;
+    } else if (cached && coop) {
+      cudaFuncGetAttributes(&a, trace_fast_kernel<true, 2>);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<true, 2>, DG_FAST_BLOCK, kFastTmaSmemBytes);
       threads = DG_FAST_BLOCK;
     } else if (cached) {
-      query(trace_fast_kernel<true, false>, DG_FAST_BLOCK);
+      query(trace_fast_kernel<true, 0>, DG_FAST_BLOCK);
     } else {
-      query(trace_fast_kernel<false, false>, DG_FAST_BLOCK);
+      query(trace_fast_kernel<false, 0>, DG_FAST_BLOCK);
     }
   } else if (cached) {
     if (full) query(trace_kernel<double, true, true>, kBlockThreads); else query(trace_kernel<double, false, true>, kBlockThreads);

@@ -58,7 +58,7 @@ def main(rounds=40, n=40000, seed=0):
         ref = None
         for m in meshes:
             slow = m.trace_batch(f, b, d, max_steps=max_steps, walker="generic")
-            for walker in (("loads", "tma") if m.has_transport_cache else ("auto",)):
+            for walker in (("loads", "tma", "coop") if m.has_transport_cache else ("auto",)):
                 fast = m.trace_batch(f, b, d, max_steps=max_steps, walker=walker)
                 for key in FIELDS:
                     x, y = getattr(fast, key), getattr(slow, key)
@@ -72,7 +72,7 @@ def main(rounds=40, n=40000, seed=0):
             pay[::5] = 0.0
             kw = dict(max_steps=max_steps, payload=pay, hole_avoidance=bool(r % 2), record_polyline=True)
             slow_full = m.trace_batch(f, b, d, walker="generic", **kw)
-            for walker in (("loads", "tma") if m.has_transport_cache else ("auto",)):
+            for walker in (("loads", "tma", "coop") if m.has_transport_cache else ("auto",)):
                 fast_full = m.trace_batch(f, b, d, walker=walker, **kw)
                 for key in FIELDS + ("payload", "poly_face", "poly_bary", "poly_seg"):
                     x, y = getattr(fast_full, key), getattr(slow_full, key)
@@ -84,7 +84,7 @@ def main(rounds=40, n=40000, seed=0):
             if r % 2:
                 kw["payload"] = pay
             slow_q = m.trace_batch(f, b, d, walker="generic", **kw)
-            for walker in (("loads", "tma") if m.has_transport_cache else ("auto",)):
+            for walker in (("loads", "tma", "coop") if m.has_transport_cache else ("auto",)):
                 fast_q = m.trace_batch(f, b, d, walker=walker, **kw)
                 keys = FIELDS + ("q",) + (("payload",) if r % 2 else ()) + (("poly_face", "poly_bary", "poly_seg") if r % 3 == 0 else ())
                 for key in keys:

@@ -65,6 +65,42 @@ __global__ void __launch_bounds__(128, 4) gather_tma(const char* rec, uint32_t n
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// (c) cooperative loads: in each of the four 256-bit load instructions, lanes 4m..4m+3 read the four
+// sectors of ONE record (owner lane 8j+m), so an instruction touches 8 lines instead of 32 -- a quarter of
+// the L1TEX->crossbar requests for the same bytes; the sectors reach their owner through shared memory.
+__global__ void __launch_bounds__(128, 4) gather_coop(const char* rec, uint32_t nrec, int iters, double* out) {
+  extern __shared__ __align__(128) char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* wbase = smem + warp * (32 * kStride);
+  char* slot = wbase + lane * kStride;
+  uint32_t idx = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u % nrec;
+  double acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    double r[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t oi = __shfl_sync(0xffffffffu, idx, 8 * j + (lane >> 2));
+      ldg256(rec + size_t(oi) * 128 + (lane & 3) * 32, r[j][0], r[j][1], r[j][2], r[j][3]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double2* w = reinterpret_cast<double2*>(wbase + (8 * j + (lane >> 2)) * kStride + (lane & 3) * 32);
+      w[0] = make_double2(r[j][0], r[j][1]);
+      w[1] = make_double2(r[j][2], r[j][3]);
+    }
+    __syncwarp();
+    double s = 0;
+    const double2* q = reinterpret_cast<const double2*>(slot);
+    double2 last;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { double2 t = q[k]; if (k < 7) s += t.x + t.y; else { s += t.x; last = t; } }
+    acc += s;
+    idx = uint32_t(__double2loint(last.y)) % nrec;
+    __syncwarp();
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 int main(int argc, char** argv) {
   const uint32_t nrec = argc > 1 ? atoi(argv[1]) : 245760;   // 31 MB, the c2 record array
   const int iters = argc > 2 ? atoi(argv[2]) : 2000;
@@ -86,15 +122,17 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const size_t smem = 4 * 32 * kStride + 64;
   cudaFuncSetAttribute(gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  for (int variant = 0; variant < 2; ++variant) {
+  cudaFuncSetAttribute(gather_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  for (int variant = 0; variant < 3; ++variant) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(e0);
       if (variant == 0) gather_ldg<<<blocks, threads>>>(rec, nrec, iters, out);
-      else gather_tma<<<blocks, threads, smem>>>(rec, nrec, iters, out);
+      else if (variant == 1) gather_tma<<<blocks, threads, smem>>>(rec, nrec, iters, out);
+      else gather_coop<<<blocks, threads, smem>>>(rec, nrec, iters, out);
       cudaEventRecord(e1);
       cudaError_t err = cudaDeviceSynchronize();
       float ms; cudaEventElapsedTime(&ms, e0, e1);
-      if (rep == 2) printf("%s: %.3f ms, %.2f G records/s (%s)\n", variant == 0 ? "4 x LDG.256 per lane" : "1 x cp.async.bulk per lane",
+      if (rep == 2) printf("%s: %.3f ms, %.2f G records/s (%s)\n", variant == 0 ? "4 x LDG.256 per lane" : variant == 1 ? "1 x cp.async.bulk per lane" : "4 x LDG.256, 4 lanes per record + smem",
                            ms, double(blocks) * threads * iters / ms / 1e6, cudaGetErrorString(err));
     }
   }

@@ -1,5 +1,5 @@
 """Device-resident timing of the GFD backward (with the forward results as its base traces) on the c2 / c3
-workloads: usage python scripts/tune_gfd.py [c2|c3] [geodesics]. DG_GFD_SIBLINGS=0 / DG_FAST_TMA=0|1 select
+workloads: usage python scripts/tune_gfd.py [c2|c3] [geodesics]. DG_GFD_SIBLINGS=0 / DG_FAST_GATHER=loads|tma|coop select
 the round-2 schedule and the gather."""
 import os, sys
 import numpy as np, torch
@@ -40,5 +40,5 @@ for _ in range(4):
     tn.append(e[0].elapsed_time(e[1]))
     assert float(jv.sum() + jp.sum()) == check
 cr = int(o["total_crossings"].item()) // 1
-print(f"{key} n={n} tma={mesh.uses_tma_gather} siblings={os.environ.get('DG_GFD_SIBLINGS', '3')} "
+print(f"{key} n={n} gather={os.environ.get('DG_FAST_GATHER', mesh.gather)} siblings={os.environ.get('DG_GFD_SIBLINGS', '3')} "
       f"forward {min(tf):.2f} ms  gfd with base {min(tg):.2f} ms  gfd alone {min(tn):.2f} ms  checksum {check:.17g}", flush=True)

@@ -15,10 +15,11 @@ FIELDS = ("face", "bary", "dir", "traced", "requested", "term", "status", "stall
 
 
 def both_walkers(m, f, b, d, **kw):
-    """General walker vs the fast walker with each gather of the crossing records (256-bit loads,
-    TMA tile::gather4; on a mesh without records both selectors run the face-record walker)."""
+    """General walker vs the fast walker with each gather of the crossing records (per-lane 256-bit
+    loads, TMA tile::gather4, cooperative loads; on a mesh without records every selector runs the
+    face-record walker)."""
     slow = m.trace_batch(f, b, d, walker="generic", **kw)
-    for walker in ("loads", "tma", "auto"):
+    for walker in ("loads", "tma", "coop", "auto"):
         fast = m.trace_batch(f, b, d, walker=walker, **kw)
         for k in FIELDS:
             x, y = getattr(fast, k), getattr(slow, k)
@@ -45,7 +46,7 @@ def test_payload_lane_of_the_fast_walker(gpu, ref, cache):
         pay[::7] = 0.0                      # zero payload = no payload (tracer.cpp:580-583)
         b[100:200] = [0.0, 1.0, 0.0]        # vertex starts: the generic path carries the payload over the fan
         slow = m.trace_batch(f, b, d, payload=pay, max_steps=max_steps, walker="generic")
-        for walker in ("loads", "tma", "auto"):
+        for walker in ("loads", "tma", "coop", "auto"):
             fast = m.trace_batch(f, b, d, payload=pay, max_steps=max_steps, walker=walker)
             for k in FIELDS + ("payload",):
                 x, y = getattr(fast, k), getattr(slow, k)
@@ -80,7 +81,7 @@ def test_transport_matrix_lane_of_the_fast_walker(gpu, ref, cache):
         for kw in (dict(), dict(payload=pay)):
             kw = dict(kw, want_q=True, max_steps=max_steps, hole_avoidance=hole)
             slow = m.trace_batch(f, b, d, walker="generic", **kw)
-            for walker in ("loads", "tma", "auto"):
+            for walker in ("loads", "tma", "coop", "auto"):
                 fast = m.trace_batch(f, b, d, walker=walker, **kw)
                 for k in FIELDS + ("q",) + (("payload",) if "payload" in kw else ()):
                     assert np.array_equal(getattr(fast, k), getattr(slow, k), equal_nan=True), (walker, k)
@@ -115,7 +116,7 @@ def test_hole_avoidance_on_the_fast_walker(gpu, ref, cache):
         pay = rng.normal(size=(len(f), 3))
         for kw in (dict(), dict(payload=pay)):
             slow = m.trace_batch(f, b, d, hole_avoidance=True, walker="generic", **kw)
-            for walker in ("loads", "tma", "auto"):
+            for walker in ("loads", "tma", "coop", "auto"):
                 fast = m.trace_batch(f, b, d, hole_avoidance=True, walker=walker, **kw)
                 for k in FIELDS + (("payload",) if kw else ()):
                     assert np.array_equal(getattr(fast, k), getattr(slow, k), equal_nan=True), (walker, k)
