@@ -48,6 +48,10 @@ struct TraceParams {
   // same crossing records at the same time: one HBM / L2 line serves all of them. 0 / 1 = plain order.
   int32_t siblings;
   int64_t sibling_stride;
+  // 1 - 1e-10 (the vertex snap threshold, tracer.cpp:155) as a kernel parameter, set by launch_fast: the fast
+  // step compares one weight of a pair against the literal and the other against this copy, because two
+  // compares with the SAME constant get fused into fmax(a, b) >= c -- nine instructions instead of two
+  double snap_hi;
   uint8_t hole_avoidance;
   uint8_t want_q;
   uint8_t he_map_ok;  // he_map is a valid tensor map of mesh.he

@@ -165,6 +165,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
   // Start-ups side by side: a warp waits for 4 idle lanes, at most DG_REFILL_PATIENCE (8) transitions.
   // Measured: c2 3.97 -> 3.77 ms, c3 24.46 -> 24.63 ms (profiles/tuning_r1.md).
   if (p.refill_min <= 0) p.refill_min = 4;
+  p.snap_hi = 1.0 - 1e-10;
   int per_sm = shape.blocks_per_sm;
   if (per_sm <= 0) {
     static std::atomic<int> cached_per_sm{0};

@@ -156,6 +156,7 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
       for (int k = 0; k < 3; ++k) hm.he[3 * size_t(f) + k] = make_halfedge_rec(mv, f, k);
   }
   TraceParams p{};
+  p.snap_hi = 1.0 - 1e-10;
   p.mesh = hm.view(cached != 0);
   p.n = n;
   p.face = face; p.bary = bary; p.dir = dir;
