@@ -215,10 +215,14 @@ DG_API int dg_transition(const dg_mesh* mesh, int which, int64_t n, const int32_
 typedef struct dg_diff_cfg {
   uint8_t memory;       /* DG_MEM_HOST / DG_MEM_DEVICE for all pointers of the call */
   uint8_t lane;         /* reserved (see DG_LANE_*) */
-  uint8_t reserved[6];
+  uint8_t schedule;     /* GFD round 2: DG_GFD_SCHEDULE_AUTO = the full-length re-traces of a sample run as
+                           sibling lanes of one warp and share every crossing-record fetch;
+                           DG_GFD_SCHEDULE_PLAIN = job order. A schedule only: same bits either way. */
+  uint8_t reserved[5];
   void* stream;
   int32_t max_steps;    /* GFD re-traces; 0 = default */
 } dg_diff_cfg;
+enum { DG_GFD_SCHEDULE_AUTO = 0, DG_GFD_SCHEDULE_PLAIN = 1 };
 
 /* Extrinsic-proxy Jacobians for n samples. rot[9n] = rotation_ep (row-major), frames
  * [DG_FRAME_DOUBLES n]; either may be NULL. Fails with DG_ERR_DEGENERATE_DIRECTION (and

@@ -262,7 +262,7 @@ class Mesh:
         check(lib().dg_ep_backward(self._handle(), int(face.numel()), ptr(face), ptr(v), ptr(end_face), ptr(end_dir),
                                    ptr(g), C.addressof(cfg), ptr(grad_v), ptr(grad_p), C.addressof(ei)), ei)
 
-    def gfd(self, face, bary, v, eps_v=None, eps_p=None, g=None, max_steps=0, out=None, base=None):
+    def gfd(self, face, bary, v, eps_v=None, eps_p=None, g=None, max_steps=0, out=None, base=None, plain_schedule=False):
         """gfd_batched_many (+ pullback_ambient when g is given), diff.cpp:273-326. `out`: a dict
         of preallocated (e.g. pinned) arrays; only the keys present are computed and copied back
         (jv, jp, degraded, frames, grad_v, grad_p, base_face, base_bary, base_dir)."""
@@ -278,7 +278,7 @@ class Mesh:
                        frames=np.zeros((n, capi.FRAME_DOUBLES)), grad_v=np.zeros((n, 3)), grad_p=np.zeros((n, 3)),
                        base_face=np.empty(n, np.int32), base_bary=np.empty((n, 3)), base_dir=np.empty((n, 3)))
         ei = C.c_int64(-1)
-        cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps))
+        cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps), schedule=int(plain_schedule))
         o = lambda k: ptr(out.get(k))
         if base is not None:  # a TraceResult of trace_batch on the same samples (gfd_batched's `trace` argument)
             check(lib().dg_gfd_jacobians_with_base(
@@ -294,12 +294,12 @@ class Mesh:
         return out
 
     def gfd_device(self, face, bary, v, eps_v, eps_p, g, jv, jp, grad_v=None, grad_p=None, degraded=None,
-                   stream=None, max_steps=0, base=None):
+                   stream=None, max_steps=0, base=None, plain_schedule=False):
         """`base`: the forward results of the same samples (dict of device tensors face / bary / dir /
         term / status, as trace_batch_device writes them): GFD then takes them as its base traces
         (the `trace` argument of gfd_batched, diff.hpp:73) instead of re-tracing them."""
         import torch
-        cfg = DiffCfg(memory=capi.MEM_DEVICE, max_steps=int(max_steps),
+        cfg = DiffCfg(memory=capi.MEM_DEVICE, max_steps=int(max_steps), schedule=int(plain_schedule),
                       stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
         ei = C.c_int64(-1)
         if base is not None:

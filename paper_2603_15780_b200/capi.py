@@ -72,7 +72,7 @@ class TraceOut(C.Structure):
 
 
 class DiffCfg(C.Structure):
-    _fields_ = [("memory", C.c_uint8), ("lane", C.c_uint8), ("reserved", C.c_uint8 * 6), ("stream", C.c_void_p),
+    _fields_ = [("memory", C.c_uint8), ("lane", C.c_uint8), ("schedule", C.c_uint8), ("reserved", C.c_uint8 * 5), ("stream", C.c_void_p),
                 ("max_steps", C.c_int32)]
 
 

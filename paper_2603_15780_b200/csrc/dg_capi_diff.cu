@@ -255,7 +255,7 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
                    b.r1_payload, b.r1_term, b.r1_status, max_steps, nullptr, stream));
   // round 2: the full-length jobs of every sample as one sibling group
   st.note(dg::launch_gfd_round2_jobs(b, stream));
-  const int group = gfd_siblings();
+  const int group = c.schedule == DG_GFD_SCHEDULE_PLAIN ? 0 : gfd_siblings();
   if (known_base) {
     st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, nullptr, nullptr,
                      b.r2_term, b.r2_status, max_steps, nullptr, stream, group ? 3 : 0, n));

@@ -96,6 +96,40 @@ def test_gfd_matches_reference(gpu, ref, fixture, n):
     assert np.array_equal(sub["jv"], ours["jv"][:64]) and np.array_equal(sub["jp"], ours["jp"][:64])
 
 
+@pytest.mark.parametrize("cache", [True, False])
+def test_gfd_sibling_schedule_and_known_base_change_no_bit(gpu, ref, cache):
+    """Round 2 of GFD runs the full-length re-traces of a sample as sibling lanes of one warp
+    (dg_diff_cfg.schedule, TraceParams::siblings: groups of 3 with the caller's forward results as
+    base traces, of 4 without). It is a schedule, not an algorithm: every output is bit-identical
+    to the plain job order, with and without a known base, on both mesh layouts, for batch sizes
+    that do not fill the last group or warp, and on an open mesh where some columns take the
+    one-sided fallback."""
+    for rm, n, eps in ((ref.RefMesh.torus(1 / 3, 1 / 6, 64, 32), 5003, None), (ref.RefMesh.icosphere(3), 61, None),
+                       (ref.RefMesh.plane(6, 6, 1.0, 0), 2500, 1e-3)):
+        a = rm.arrays()
+        m = gpu.Mesh(a["xyz"], a["tri"], transport_cache=cache)
+        f, b, d = rm.sample_queries(21, n, 0.05, 0.7)
+        base = m.trace_batch(f, b, d)
+        if eps is not None:   # traces that hit the boundary end 1e-9 before it instead: their + perturbations leave the mesh
+            hit = base.term == 1
+            d[hit] *= ((base.traced[hit] - 1e-9) / base.requested[hit])[:, None]
+            base = m.trace_batch(f, b, d)
+        keep = (base.term == 0) & (base.status == 0)
+        if eps is not None:   # seeds (eps-length) must stay on the open mesh
+            P = rm.embed(f, b)
+            keep &= (P[:, :2].min(1) > 0.02) & (P[:, :2].max(1) < 0.98)
+        f, b, d = f[keep], b[keep], d[keep]
+        base = m.trace_batch(f, b, d)
+        g = unit_rows(np.random.default_rng(3), len(f))
+        kw = dict(g=g) if eps is None else dict(g=g, eps_v=eps, eps_p=eps)
+        want = m.gfd(f, b, d, plain_schedule=True, **kw)
+        for got in (m.gfd(f, b, d, **kw), m.gfd(f, b, d, base=base, **kw), m.gfd(f, b, d, base=base, plain_schedule=True, **kw)):
+            for k in ("jv", "jp", "degraded", "frames", "grad_v", "grad_p"):
+                assert np.array_equal(got[k], want[k], equal_nan=True), k
+        if eps is not None:
+            assert want["degraded"].any(), "fixture must exercise the fallback"
+
+
 def test_gfd_plane_is_identity(gpu, ref):
     """test_diff.cpp:89-112: on a flat mesh both Jacobians are the frame change of the identity."""
     rm = ref.RefMesh.plane(12, 12, 4.0, 5)
