@@ -158,7 +158,7 @@ cudaError_t launch_one(const TraceParams& p_in, LaunchShape shape, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <bool kCached, int kTma, int kPay = 0>
+template <bool kCached, int kTma, int kPay = 0, bool kDense = false>
 cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t stream) {
   constexpr size_t smem = kTma ? size_t(kFastTmaSmemBytes) : 0;
   TraceParams p = p_in;
@@ -171,7 +171,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
     static std::atomic<int> cached_per_sm{0};
     per_sm = cached_per_sm.load(std::memory_order_relaxed);
     if (per_sm <= 0) {
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma, kPay>, DG_FAST_BLOCK, smem);
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma, kPay, kDense>, DG_FAST_BLOCK, smem);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
       cached_per_sm.store(per_sm, std::memory_order_relaxed);
@@ -181,7 +181,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
   const long long needed = (p.n + DG_FAST_BLOCK - 1) / DG_FAST_BLOCK;
   if (blocks > needed) blocks = needed;
   if (blocks < 1) blocks = 1;
-  trace_fast_kernel<kCached, kTma, kPay><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
+  trace_fast_kernel<kCached, kTma, kPay, kDense><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -239,7 +239,10 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
          : gather == 2 ? launch_fast<true, 2, kPay>(p, shape, stream)
                        : launch_fast<true, 0, kPay>(p, shape, stream);
   };
-  if (!needs_full && shape.walker != 1 && fast_walk_enabled()) return fast(std::integral_constant<int, 0>{});
+  if (!needs_full && shape.walker != 1 && fast_walk_enabled()) {
+    if (p.mesh.he && gather == 0 && p.siblings > 1) return launch_fast<true, 0, 0, true>(p, shape, stream);
+    return fast(std::integral_constant<int, 0>{});
+  }
   // a payload to transport, hole avoidance, a polyline to record -- anything but the transport matrix:
   // the fast walker carries the payload along, writes one polyline point per step and leaves boundary
   // events to the full Tracer behind it
