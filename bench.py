@@ -48,8 +48,8 @@ def make_workload(key, n, seed):
 
 
 class ClockSampler:
-    """SM clock and throttle reasons sampled DURING the timed region: NVML in a thread (every 5 ms, so that
-    a 20 ms region still gets samples), `nvidia-smi -lms` as the fallback when NVML cannot be loaded."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML in a thread (every 2 ms plus the query time,
+    so that a 20 ms region still gets samples), `nvidia-smi -lms` as the fallback when NVML cannot be loaded."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -81,16 +81,19 @@ class ClockSampler:
                      "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
         self.mx.append(float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)))
 
-    def _poll_nvml(self):
+    def _sample_nvml(self):
         nv = self.nvml
+        try:
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)))
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+            self.seen.update(nm for nm, bit in self.bits.items() if mask & bit)
+        except Exception:
+            pass
+
+    def _poll_nvml(self):
         while not self.stop.is_set():
-            try:
-                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
-                self.seen.update(nm for nm, bit in self.bits.items() if mask & bit)
-            except Exception:
-                pass
-            self.stop.wait(0.005)
+            self._sample_nvml()
+            self.stop.wait(0.002)
 
     def _read_smi(self):
         for line in self.proc.stdout:
@@ -125,6 +128,8 @@ class ClockSampler:
         if self.nvml:
             self.stop.set()
             self.t.join(timeout=2)
+            if not self.sm:          # a region shorter than one NVML round trip: the clock it ends on
+                self._sample_nvml()
         elif self.proc:
             time.sleep(0.15)
             self.proc.terminate()
@@ -140,6 +145,19 @@ def measured_peak():
     if os.path.exists(p):
         return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def gather_roofline(mesh, crossings_per_s):
+    """Measured gather rates (G records/s) of scripts/micro/gather_bench.cu / gather4_bench.cu on B200 at 31 MB,
+    384 MB and 1.5 GB of records, per gather; the nearest size at or above the mesh's record array is the ceiling."""
+    table = {"loads": ((31e6, 67.0), (384e6, 16.5), (1.5e9, 10.3)), "coop": ((31e6, 86.6), (384e6, 65.6), (1.5e9, 40.9)),
+             "tma": ((31e6, 106.0), (384e6, 65.0), (1.5e9, 40.0))}
+    if not mesh.has_transport_cache:
+        return None
+    rec_bytes = 3 * mesh.nf * 128
+    peak = next((r for size, r in table[mesh.gather] if rec_bytes <= size * 1.05), table[mesh.gather][-1][1])
+    return {"gather": mesh.gather, "record_bytes": rec_bytes, "achieved_grecords_per_s": crossings_per_s / 1e9,
+            "peak_grecords_per_s": peak, "frac": crossings_per_s / 1e9 / peak, "source": "scripts/micro/gather_bench.cu (profiles/tuning_r1.md)"}
 
 
 def profile_traffic(workload):
@@ -408,7 +426,11 @@ def run_ours(args):
                              "peak_source": peak_src,
                              "algorithmic_bytes_per_launch": alg_bytes,
                              "note": "dependent-gather walk: bound by FP64 issue + L2 latency, not HBM bandwidth (DESIGN.md)",
-                             "registers": info["registers"], "blocks_per_sm": info["blocks_per_sm"]},
+                             "registers": info["registers"], "blocks_per_sm": info["blocks_per_sm"],
+                             # the access pattern's own ceiling: random 128-byte records, one per lane per round, dependent
+                             # next index, measured with scripts/micro/gather_bench.cu at this record-array size with the
+                             # gather this mesh uses (profiles/tuning_r1.md); one record = one face crossing
+                             "gather": gather_roofline(mesh, crossings_per_step / t_trace)},
                 "e2e": {"value": e2e_value, "unit": "face-crossings/s", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "ms_per_step": float(e2e_ms.item())},
                 "gpu_launches": launches, "clocks": clocks.summary()}
