@@ -319,8 +319,8 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
     } else {
       // Measured (profiles/tuning_r1.md, scripts/sweep_cache_policy.py): the walker over crossing
       // records beats the one over face records at every mesh size once the records are gathered
-      // through TMA beyond the load path's TLB reach (250 MB; dg_trace_kernel.cu), so AUTO only guards
-      // capacity.
+      // one request per record beyond 250 MB (cooperative loads or TMA; gather_mode, dg_trace_kernel.cu),
+      // so AUTO only guards capacity.
       cache = 3 * F * sizeof(dg::HalfEdgeRec) <= (size_t(16) << 30);
     }
   }
