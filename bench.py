@@ -434,6 +434,20 @@ def run_ours(args):
                 "e2e": {"value": e2e_value, "unit": "face-crossings/s", "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "ms_per_step": float(e2e_ms.item())},
                 "gpu_launches": launches, "clocks": clocks.summary()}
+        if scheme == "gfd":
+            # the kernel that takes most of a GFD step: round 2, three full-length re-traces per sample as sibling
+            # groups (+ n eps-length jobs). Its duration is rank 0's backward time (job builders, seeds and assembly
+            # are < 2 % of it, profiles/r1_launches_bench_c3_summary.txt); algorithmic bytes as for the forward walk.
+            t_bwd = (float(np.mean(step_ms)) - float(np.mean(tr_ms))) * 1e-3
+            alg2 = 3 * crossings_per_step * BYTES_PER_CROSSING + 4 * n * BYTES_PER_GEODESIC
+            tr2 = profile_traffic(args.workload + "_gfd_round2")
+            info2 = dg.kernel_info(False, False, cached=mesh.has_transport_cache, dense=True)
+            line["roofline_gfd_round2"] = {"bound": "hbm", "achieved": alg2 / t_bwd / 1e9, "peak": peak, "unit": "GB/s",
+                                           "frac": alg2 / t_bwd / 1e9 / peak,
+                                           "traffic": tr2["dram_bytes_per_launch"] if tr2 else None,
+                                           "kernel": "trace_fast_kernel<crossing records, 256-bit loads, sibling groups of 3>",
+                                           "algorithmic_bytes_per_launch": alg2, "registers": info2["registers"],
+                                           "blocks_per_sm": info2["blocks_per_sm"]}
         if not args.no_cpu and world == 1:
             try:
                 cps, gps, sample, threads, _, _, _ = cpu_reference(xyz, tri, f, b, d, q, scheme)

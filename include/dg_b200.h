@@ -192,6 +192,7 @@ DG_API int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in,
 
 /* Registers per thread, resident CTAs per SM and CTA size of a tracer kernel variant.
  * full: bit 2 = the TMA-gather variant of the fast walker, bit 3 = its cooperative-loads variant,
+ *       bit 4 = its sibling-schedule instantiation (6 CTAs per SM),
  *       bit 0 = payload / transport matrix / hole avoidance / polyline support compiled in,
  *       bit 1 = transport-cache variant. */
 DG_API void dg_trace_kernel_info(int use_f32, int full, int* regs, int* blocks_per_sm,

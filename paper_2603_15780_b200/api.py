@@ -386,8 +386,9 @@ class Batch:
         return out
 
 
-def kernel_info(use_f32=False, full=False, cached=False, tma=False, coop=False):
+def kernel_info(use_f32=False, full=False, cached=False, tma=False, coop=False, dense=False):
     regs, bps, bt = C.c_int(0), C.c_int(0), C.c_int(0)
-    lib().dg_trace_kernel_info(int(use_f32), int(full) | (int(cached) << 1) | (int(tma) << 2) | (int(coop) << 3), C.addressof(regs), C.addressof(bps),
+    lib().dg_trace_kernel_info(int(use_f32), int(full) | (int(cached) << 1) | (int(tma) << 2) | (int(coop) << 3) | (int(dense) << 4),
+                               C.addressof(regs), C.addressof(bps),
                                C.addressof(bt))
     return dict(registers=regs.value, blocks_per_sm=bps.value, block_threads=bt.value)

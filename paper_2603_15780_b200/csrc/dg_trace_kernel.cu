@@ -257,7 +257,8 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
 void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads) {
   cudaFuncAttributes a{};
   int per_sm = 0, threads = kBlockThreads;
-  const bool full = variant & 1, cached = (variant & 2) && !use_f32, tma = (variant & 4) != 0, coop = (variant & 8) != 0;
+  const bool full = variant & 1, cached = (variant & 2) && !use_f32, tma = (variant & 4) != 0, coop = (variant & 8) != 0,
+             dense = (variant & 16) != 0;
   auto query = [&](auto kernel, int block) {
     cudaFuncGetAttributes(&a, kernel);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0);
@@ -270,6 +271,8 @@ void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm,
       cudaFuncGetAttributes(&a, trace_fast_kernel<true, 1>);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<true, 1>, DG_FAST_BLOCK, kFastTmaSmemBytes);
       threads = DG_FAST_BLOCK;
+    } else if (cached && dense) {
+      query(trace_fast_kernel<true, 0, 0, true>, DG_FAST_BLOCK);
     } else if (cached && coop) {
       cudaFuncGetAttributes(&a, trace_fast_kernel<true, 2>);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<true, 2>, DG_FAST_BLOCK, kFastTmaSmemBytes);
