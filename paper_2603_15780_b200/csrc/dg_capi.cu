@@ -402,7 +402,8 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
                     {nullptr, out->payload, out->payload ? 24 * N : 0, 0},
                     {nullptr, out->transport, out->transport ? 72 * N : 0, 0},
                     {nullptr, out->npoints, out->npoints ? 4 * N : 0, 0},
-                    {nullptr, out->crossings, out->crossings ? 4 * N : 0, 0},
+                    // (a mapped call sums the batch total on the host from this array: it is written whenever the total is asked for)
+                    {nullptr, out->crossings, (out->crossings || out->total_crossings) ? 4 * N : 0, 0},
                     {nullptr, out->term, out->term ? N : 0, 0},
                     {nullptr, out->status, out->status ? N : 0, 0},
                     {nullptr, out->stall, out->stall ? N : 0, 0},
@@ -424,12 +425,13 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
     DG_CUDA(cudaMallocHost(&mesh->small_pin, cap));
     DG_CUDA(cudaMalloc(&mesh->small_dev, cap));
     mesh->small_cap = cap;
+    mesh->small_cursors_clean = false;
   }
   char* hp = static_cast<char*>(mesh->small_pin);
   char* dp = static_cast<char*>(mesh->small_dev);
   // The smallest batches skip both copies: the pinned block is mapped into the device's address space (unified
   // addressing), the kernel reads its queries from it and writes its results into it over PCIe, and only the 16
-  // bytes of work counters live in device memory (atomics). Measured (tests/cpp/bench_small_batch.cpp, us per call
+  // bytes of work cursors live in device memory (atomics). Measured (tests/cpp/bench_small_batch.cpp, us per call
   // with the transport matrix, copies -> mapped): 1 seed 40.7 -> 30.8, 50 seeds 70.3 -> 65.4, 1 000 seeds 112.7 -> 111.7,
   // 8 000 seeds 524 -> 596: mapped up to 256 queries. DG_SMALL_MAPPED_MAX overrides the limit.
   static const int64_t mapped_max = [] {
@@ -440,8 +442,18 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   std::memset(hp, 0, 16);
   for (auto& f : fin) if (f.bytes) std::memcpy(hp + f.off, f.src, f.bytes);
   cudaStream_t stream = mesh->stream;
-  if (mapped) DG_CUDA(cudaMemsetAsync(dp, 0, 16, stream));
-  else DG_CUDA(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, stream));
+  // Mapped calls alternate between two work cursors in device memory; every launch zeroes the one the NEXT call
+  // uses (TraceParams::clear_word), so a call is one kernel launch and one synchronisation -- no memset, no copy.
+  // Anything that may have left the cursors dirty (first use, reallocation, a copied call, an error) resets both.
+  unsigned long long* cursors = reinterpret_cast<unsigned long long*>(dp);
+  const unsigned turn = mesh->small_calls++ & 1u;
+  if (mapped) {
+    if (!mesh->small_cursors_clean) DG_CUDA(cudaMemsetAsync(dp, 0, 16, stream));
+    mesh->small_cursors_clean = false;   // set again once this call has completed
+  } else {
+    mesh->small_cursors_clean = false;
+    DG_CUDA(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, stream));
+  }
 
   dg::TraceParams p{};
   mesh->bind(p);
@@ -465,9 +477,10 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   p.o_term = reinterpret_cast<uint8_t*>(dout(9));
   p.o_status = reinterpret_cast<uint8_t*>(dout(10));
   p.o_stall = reinterpret_cast<uint8_t*>(dout(11));
-  p.queue_head = reinterpret_cast<unsigned long long*>(dp);
-  // mapped: the sum of the batch is accumulated next to the work cursor in device memory and read back on its own
-  p.total_crossings = fout[12].bytes ? reinterpret_cast<unsigned long long*>(mapped ? dp + 8 : dp + fout[12].off) : nullptr;
+  p.queue_head = mapped ? cursors + turn : cursors;
+  p.clear_word = mapped ? cursors + (turn ^ 1u) : nullptr;
+  // mapped: the sum of the batch is taken on the host from the per-query counts
+  p.total_crossings = (fout[12].bytes && !mapped) ? reinterpret_cast<unsigned long long*>(dp + fout[12].off) : nullptr;
   p.max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
   p.refill_min = 0;
   p.hole_avoidance = c.hole_avoidance;
@@ -475,13 +488,19 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   if (p.total_crossings && !mapped) DG_CUDA(cudaMemsetAsync(p.total_crossings, 0, 8, stream));
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || out->payload || out->transport;
   DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, needs_full, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm), int(c.walker)}, stream));
-  if (mapped) {
-    if (fout[12].bytes) DG_CUDA(cudaMemcpyAsync(hp + fout[12].off, dp + 8, 8, cudaMemcpyDeviceToHost, stream));
-  } else if (total > out_begin) {
+  if (!mapped && total > out_begin)
     DG_CUDA(cudaMemcpyAsync(hp + out_begin, dp + out_begin, total - out_begin, cudaMemcpyDeviceToHost, stream));
-  }
   DG_CUDA(cudaStreamSynchronize(stream));
-  for (auto& f : fout) if (f.bytes) std::memcpy(f.dst, hp + f.off, f.bytes);
+  if (mapped) {
+    mesh->small_cursors_clean = true;
+    if (fout[12].bytes) {
+      uint64_t sum = 0;
+      const int32_t* cr = reinterpret_cast<const int32_t*>(hp + fout[8].off);
+      for (size_t i = 0; i < N; ++i) sum += uint64_t(cr[i]);
+      std::memcpy(hp + fout[12].off, &sum, 8);
+    }
+  }
+  for (auto& f : fout) if (f.bytes && f.dst) std::memcpy(f.dst, hp + f.off, f.bytes);
   return DG_OK;
 }
 

@@ -38,6 +38,8 @@ struct dg_mesh {
   mutable void* small_pin = nullptr;
   mutable void* small_dev = nullptr;
   mutable size_t small_cap = 0;
+  mutable unsigned small_calls = 0;      // parity picks the work cursor of a mapped small-batch call
+  mutable bool small_cursors_clean = false;
   // large plain host-mode batches run through a resident batch (dg_capi_batch.cu) owned by the mesh
   mutable std::mutex host_batch_mu;
   mutable struct dg_batch* host_batch = nullptr;

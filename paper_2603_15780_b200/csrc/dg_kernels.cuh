@@ -39,6 +39,7 @@ struct TraceParams {
   double* poly_bary;
   double* poly_seg;
   unsigned long long* queue_head;       // work-stealing cursor, zeroed before the launch
+  unsigned long long* clear_word;       // optional: a word this launch zeroes (the cursor of the NEXT small-batch call)
   unsigned long long* total_crossings;  // optional: += sum of crossings of the batch
   int32_t max_steps;
   int32_t refill_min;  // refill a warp once this many lanes are idle (0 = the walker's default)

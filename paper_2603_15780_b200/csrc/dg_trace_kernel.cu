@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(kBlockThreads, kFull ? DG_TRACE_MIN_BLOCKS_FUL
   Tracer<S, kFull, kCached> T(p.mesh, p.max_steps, p.hole_avoidance != 0);
   const unsigned lane = threadIdx.x & 31u;
   const unsigned long long n = (unsigned long long)p.n;
+  if (p.clear_word && blockIdx.x == 0 && threadIdx.x == 0) *p.clear_word = 0ull;
   bool live = false;
   bool exhausted = false;  // warp-uniform: the queue has no more work
   int64_t q = -1;
