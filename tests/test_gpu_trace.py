@@ -169,6 +169,30 @@ def test_empty_and_single(gpu, ref):
     assert_trace_equal(r, h, 1)
 
 
+def test_host_mode_paths_by_batch_size_agree(gpu, ref):
+    """Host-mode dg_trace_batch picks its plumbing by batch size -- up to 256 queries the kernel works
+    on the mapped pinned block (alternating work cursors, no copies), up to 8 192 one packed copy
+    each way, from 65 536 the sliced copy/compute pipeline -- and none of it may show in the
+    results: every prefix of a batch equals the same rows of the whole batch, call after call
+    (both cursor parities), with and without the transport matrix, totals included."""
+    rm = ref.RefMesh.torus(1 / 3, 1 / 6, 48, 24)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(77, 70000, 0.05, 1.5)
+    fields = ("face", "bary", "dir", "traced", "requested", "term", "status", "stall", "crossings")
+    for want_q in (False, True):
+        whole = m.trace_batch(f, b, d, want_q=want_q)
+        assert whole.total_crossings == int(whole.crossings.sum())
+        for k in (1, 2, 50, 255, 256, 257, 300, 8192, 8193, 65536):
+            for _ in range(3 if k <= 300 else 1):
+                part = m.trace_batch(f[:k], b[:k], d[:k], want_q=want_q)
+                for key in fields + (("q",) if want_q else ()):
+                    assert np.array_equal(getattr(part, key), getattr(whole, key)[:k], equal_nan=True), (k, key)
+                assert part.total_crossings == int(whole.crossings[:k].sum()), k
+    theirs = rm.trace_batch(f[:300], b[:300], d[:300])
+    part = m.trace_batch(f[:300], b[:300], d[:300])
+    assert np.array_equal(part.face, theirs.face) and np.array_equal(part.term, theirs.term)
+
+
 def test_invalid_batch_arguments(gpu, ref):
     m = gpu_mesh(gpu, ref.RefMesh.icosphere(1))
     with pytest.raises(gpu.DgError) as e:
