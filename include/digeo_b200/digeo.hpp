@@ -1,8 +1,11 @@
 // digeo.hpp -- host-side C++ surface of the B200 tracer, source-compatible with the reference's
 // public API for the hot path (proj/include/digeo/{geometry,mesh,tracer,diff}.hpp): the same
-// namespace, type names, field names, function signatures and exception types, so that a caller
-// such as gradcheck.cpp:70-89, opt.cpp:309 or digeo_main.cpp:143-162 recompiles against this
-// header and links libdigeo_host.so + libdigeo_b200.so instead of digeo_core.
+// namespace, type names, field names, function signatures and exception types. The forwarding
+// headers include/digeo/{geometry,mesh,tracer,diff}.hpp put it under the reference's include
+// paths, so the reference's own callers -- gradcheck.cpp, oracles.cpp, io.cpp, opt.cpp and
+// tests/acceptance.cpp, UNMODIFIED -- compile against it and link libdigeo_host.so +
+// libdigeo_b200.so instead of digeo_core (tests/refdrop/Makefile builds exactly that and
+// tests/test_gpu_refdrop.py runs it on the GPU).
 //
 // Everything that computes goes through the C-ABI in dg_b200.h (CUDA, sm_100a); there is no CPU
 // tracing path behind these functions. What stays on the host is what the reference keeps in
@@ -10,6 +13,7 @@
 // accessor algebra on an already computed JacobianPair (pullback).
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -56,6 +60,15 @@ template <class S> Vec3<S> normalized(const Vec3<S>& v) {
   const S n = norm(v);
   return n > S(0) ? v / n : Vec3<S>{};
 }
+// geometry.hpp:50-67: unsigned / signed angles (atan2 forms) and the Rodrigues rotation about a unit axis
+template <class S> S angle_between(const Vec3<S>& a, const Vec3<S>& b) { return std::atan2(norm(cross(a, b)), dot(a, b)); }
+template <class S> S signed_angle(const Vec3<S>& a, const Vec3<S>& b, const Vec3<S>& axis) {
+  return std::atan2(dot(cross(a, b), axis), dot(a, b));
+}
+template <class S> Vec3<S> rotate_about(const Vec3<S>& v, const Vec3<S>& axis, S angle) {
+  const S c = std::cos(angle), s = std::sin(angle);
+  return v * c + cross(axis, v) * s + axis * (dot(axis, v) * (S(1) - c));
+}
 using Vec3d = Vec3<double>;
 using Vec3f = Vec3<float>;
 
@@ -85,12 +98,50 @@ struct Mat2 {  // row-major
   double max_abs() const { return std::fmax(std::fmax(std::fabs(a), std::fabs(b)), std::fmax(std::fabs(c), std::fabs(d))); }
 };
 
+// geometry.hpp:136: coefficients of v on the in-plane basis {e1, e2} through the 2x2 Gram system
+inline std::array<double, 2> plane_coefficients(const Vec3d& e1, const Vec3d& e2, const Vec3d& v) {
+  const double g11 = dot(e1, e1), g12 = dot(e1, e2), g22 = dot(e2, e2);
+  const double r1 = dot(e1, v), r2 = dot(e2, v);
+  const double det = g11 * g22 - g12 * g12;
+  return {(g22 * r1 - g12 * r2) / det, (g11 * r2 - g12 * r1) / det};
+}
+
+// geometry.hpp:146-185: the reference's deterministic generator -- xoshiro256** seeded through splitmix64, 53-bit
+// uniform() -- so that samplers compiled against this header draw the reference's streams
+struct Rng {
+  explicit Rng(std::uint64_t seed) {
+    for (auto& w : s_) {   // splitmix64
+      std::uint64_t z = (seed += 0x9e3779b97f4a7c15ULL);
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+      w = z ^ (z >> 31);
+    }
+  }
+  std::uint64_t next_u64() {
+    const std::uint64_t result = rotl(s_[1] * 5, 7) * 9, t = s_[1] << 17;
+    s_[2] ^= s_[0]; s_[3] ^= s_[1]; s_[1] ^= s_[2]; s_[0] ^= s_[3]; s_[2] ^= t;
+    s_[3] = rotl(s_[3], 45);
+    return result;
+  }
+  double uniform() { return double(next_u64() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  int uniform_int(int n) { return int(next_u64() % std::uint64_t(n)); }  // in [0, n)
+
+ private:
+  static std::uint64_t rotl(std::uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  std::uint64_t s_[4];
+};
+
 struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ParseError : Error { using Error::Error; };
 struct NonManifoldError : Error { using Error::Error; };
 struct DegenerateFaceError : Error { using Error::Error; };
 struct NumericalStall : Error { using Error::Error; };
 struct DegenerateDirection : Error { using Error::Error; };
+struct NotOnSphere : Error { using Error::Error; };
+struct NotTangent : Error { using Error::Error; };
+struct StepTooLarge : Error { using Error::Error; };
+struct MaxIterations : Error { using Error::Error; };
 struct InvalidArgs : Error { using Error::Error; };
 struct IOError : Error { using Error::Error; };
 struct BoundaryHit : Error { using Error::Error; };
@@ -166,6 +217,7 @@ Mesh concat_meshes(const Mesh& a, const Mesh& b);
 Vec3d embed(const SurfacePoint& p, const Mesh& m);
 PointClassification classify(const SurfacePoint& p, double tol = kBaryTol);
 bool bary_valid(const Vec3d& b, double tol = 1e-9);
+Vec3d project_to_face(const Mesh& m, int f, const Vec3d& q);  // barycentrics of the closest point of face f (mesh.cpp:233)
 double total_angle(int vertex, const Mesh& m);
 
 // ---- tracer.hpp --------------------------------------------------------------------------

@@ -281,9 +281,12 @@ class Mesh:
         cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps), schedule=int(plain_schedule))
         o = lambda k: ptr(out.get(k))
         if base is not None:  # a TraceResult of trace_batch on the same samples (gfd_batched's `trace` argument)
+            # converted copies are bound to locals: they must outlive the C call
+            bface, bbary, bdir = _i32(base.face), _f64(base.bary), _f64(base.dir)
+            bterm, bstatus = np.ascontiguousarray(base.term, np.uint8), np.ascontiguousarray(base.status, np.uint8)
             check(lib().dg_gfd_jacobians_with_base(
-                h, n, ptr(face), ptr(bary), ptr(v), ptr(_i32(base.face)), ptr(_f64(base.bary)), ptr(_f64(base.dir)),
-                ptr(base.term), ptr(base.status), float(eps_v), float(eps_p), ptr(g), C.addressof(cfg), o("jv"), o("jp"),
+                h, n, ptr(face), ptr(bary), ptr(v), ptr(bface), ptr(bbary), ptr(bdir),
+                ptr(bterm), ptr(bstatus), float(eps_v), float(eps_p), ptr(g), C.addressof(cfg), o("jv"), o("jp"),
                 o("degraded"), o("frames"), o("grad_v") if g is not None else None,
                 o("grad_p") if g is not None else None, C.addressof(ei)), ei)
             return out

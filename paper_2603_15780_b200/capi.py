@@ -134,8 +134,12 @@ def ptr(a):
     if a is None:
         return None
     if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("ptr(): array is not C-contiguous")
         return a.ctypes.data
-    return a.data_ptr()  # torch.Tensor
+    if not a.is_contiguous():  # torch.Tensor
+        raise ValueError("ptr(): tensor is not contiguous")
+    return a.data_ptr()
 
 
 def device_count() -> int:

@@ -5,6 +5,7 @@
 #include "digeo_b200/digeo.hpp"
 
 #include <algorithm>
+#include <limits>
 #include <cstdlib>
 #include <fstream>
 #include <sstream>
@@ -242,6 +243,30 @@ bool bary_valid(const Vec3d& b, double tol) {
   return true;
 }
 double total_angle(int vertex, const Mesh& m) { return m.vertex_total_angle[vertex]; }
+
+// mesh.cpp:233-261: barycentrics of the point of face f closest to q -- the in-plane coefficients when they lie in
+// the simplex, else the nearest of the three clamped edge projections (edge k is opposite corner k; first minimum wins).
+Vec3d project_to_face(const Mesh& m, int f, const Vec3d& q) {
+  const auto& c = m.faces[f];
+  const Vec3d corner[3] = {m.vertices[c[0]], m.vertices[c[1]], m.vertices[c[2]]};
+  const auto coef = plane_coefficients(corner[1] - corner[0], corner[2] - corner[0], q - corner[0]);
+  if (coef[0] >= 0 && coef[1] >= 0 && coef[0] + coef[1] <= 1.0) return {1.0 - coef[0] - coef[1], coef[0], coef[1]};
+  Vec3d nearest{1, 0, 0};
+  double nearest_d2 = std::numeric_limits<double>::infinity();
+  for (int k = 0; k < 3; ++k) {
+    const int i = (k + 1) % 3, j = (k + 2) % 3;
+    const Vec3d along = corner[j] - corner[i];
+    const double t = std::clamp(dot(q - corner[i], along) / norm2(along), 0.0, 1.0);
+    const double d2 = norm2(q - (corner[i] + along * t));
+    if (d2 < nearest_d2) {
+      nearest_d2 = d2;
+      nearest = Vec3d{0, 0, 0};
+      nearest[i] = 1.0 - t;
+      nearest[j] = t;
+    }
+  }
+  return nearest;
+}
 
 // ------------------------------------------------------------------------------ tracing
 int default_max_steps(const Mesh& m) { return int(10.0 * std::sqrt(double(m.face_count()))) + 100; }

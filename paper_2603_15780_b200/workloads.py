@@ -105,3 +105,52 @@ def vertex_edge_queries(xyz, tri, n: int, length: float, seed: int = 5):
     d = xyz[tri[face, 1]] - xyz[tri[face, 0]]
     d *= (length / np.linalg.norm(d, axis=1))[:, None]
     return face, bary, d
+
+
+def concat(parts):
+    """concat_meshes semantics (mesh.cpp:199-206) on arrays: vertices appended, face vertex ids offset,
+    faces in part order. Returns xyz, tri, vertex offsets [len+1], face offsets [len+1]."""
+    voff = np.cumsum([0] + [len(x) for x, _ in parts])
+    foff = np.cumsum([0] + [len(t) for _, t in parts])
+    xyz = np.concatenate([x for x, _ in parts])
+    tri = np.concatenate([t.astype(np.int64) + voff[i] for i, (_, t) in enumerate(parts)]).astype(np.int32)
+    return xyz, tri, voff, foff
+
+
+def config4(meshes: int = 64, queries_per_mesh: int = 65536, seed: int = 4):
+    """Config 4: `meshes` components of 10 k - 200 k faces (six noisy tori of uniformly drawn
+    face count to one bumpy sphere and one icosphere; a fixed seed-chosen list, about 6 M faces in all, each scaled by a factor in [0.5, 1.5]) concatenated into ONE
+    mesh; `queries_per_mesh` queries on each, lengths log-uniform in [0.01, 2] x that component's bbox
+    diagonal (divergence stress). Returns xyz, tri, face, bary, dir, face offsets."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for i in range(meshes):
+        kind = i % 8
+        if kind == 0:
+            xyz, tri = icosphere(int(rng.integers(5, 7)))                         # 20 k / 82 k faces
+        elif kind == 1:
+            xyz, tri = bumpy_sphere(6, amplitude=0.05 + 0.05 * rng.random())      # 82 k
+        else:
+            na = int(round(np.sqrt(rng.uniform(10_000, 200_000))))                # na x na/2 x 2 = 10 k - 200 k faces
+            xyz, tri = torus(1 / 3, 1 / 6, na, na // 2, noise=0.05, seed=i)
+        parts.append((xyz * (0.5 + rng.random()), tri))
+    xyz, tri, voff, foff = concat(parts)
+    fs, bs, ds = [], [], []
+    for i, (x, t) in enumerate(parts):
+        diag = bbox_diagonal(x)
+        f, b, d = sample_queries(x, t, queries_per_mesh, (0.01 * diag, 2.0 * diag), seed=100 + i)
+        fs.append(f + np.int32(foff[i])); bs.append(b); ds.append(d)
+    return xyz, tri, np.concatenate(fs).astype(np.int32), np.concatenate(bs), np.concatenate(ds), foff
+
+
+def config5(n: int, seed: int = 5, noise: float = 0.0):
+    """Config 5: the 1 M-face torus, n queries of length 5 x the outer diameter (= 5.0
+    for make_torus(1/3, 1/6)), the first half exactly at vertices aimed exactly along an incident edge,
+    the second half random. To be traced with max_steps = 200 000 on both sides."""
+    xyz, tri = torus(1 / 3, 1 / 6, 1000, 500, noise=noise, seed=7)
+    fv, bv, dv = vertex_edge_queries(xyz, tri, n // 2, 5.0, seed=seed)
+    fr, br, dr = sample_queries(xyz, tri, n - n // 2, 5.0, seed=seed + 4)
+    return xyz, tri, np.concatenate([fv, fr]), np.concatenate([bv, br]), np.concatenate([dv, dr])
+
+
+C5_MAX_STEPS = 200_000

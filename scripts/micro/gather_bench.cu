@@ -4,6 +4,8 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_bench gather_bench.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ void ldg256(const void* p, double& a, double& b, double& c, double& d) {
@@ -123,7 +125,9 @@ int main(int argc, char** argv) {
   const size_t smem = 4 * 32 * kStride + 64;
   cudaFuncSetAttribute(gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaFuncSetAttribute(gather_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const int only = argc > 3 ? atoi(argv[3]) : -1;   // one variant, machine-readable: bench.py's gather ceiling
   for (int variant = 0; variant < 3; ++variant) {
+    if (only >= 0 && variant != only) continue;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(e0);
       if (variant == 0) gather_ldg<<<blocks, threads>>>(rec, nrec, iters, out);
@@ -132,6 +136,11 @@ int main(int argc, char** argv) {
       cudaEventRecord(e1);
       cudaError_t err = cudaDeviceSynchronize();
       float ms; cudaEventElapsedTime(&ms, e0, e1);
+      if (rep == 2 && only >= 0) {
+        printf("{\"variant\": %d, \"records\": %u, \"ms\": %.4f, \"grecords_per_s\": %.4f, \"cuda\": \"%s\"}\n", variant, nrec, ms,
+               double(blocks) * threads * iters / ms / 1e6, cudaGetErrorString(err));
+        continue;
+      }
       if (rep == 2) printf("%s: %.3f ms, %.2f G records/s (%s)\n", variant == 0 ? "4 x LDG.256 per lane" : variant == 1 ? "1 x cp.async.bulk per lane" : "4 x LDG.256, 4 lanes per record + smem",
                            ms, double(blocks) * threads * iters / ms / 1e6, cudaGetErrorString(err));
     }
