@@ -16,7 +16,8 @@
  *   dg_ep_backward        <- ep_jacobians + pullback_ambient   proj/src/diff.cpp:44-66,328-354
  *   dg_gfd_jacobians      <- gfd_batched_many / gfd_batched / gfd_jacobian_v/p
  *                                                              proj/src/diff.cpp:208-326
- *   dg_pullback           <- pullback / pullback_ambient       proj/src/diff.cpp:328-354
+ *                            (pullback of g is fused into dg_ep_backward / dg_gfd_jacobians: pass g)
+ *   dg_set_devices        <- the fork/join of trace_batch      proj/src/tracer.cpp:596-603
  *   dg_batch_*            <- the call pair trace_batch -> EP loop / gfd_batched_many of one
  *                            training step                        proj/src/gradcheck.cpp:70-89
  *
@@ -85,6 +86,20 @@ DG_API const char* dg_version(void);
 DG_API int dg_device_count(void);          /* 0 when no CUDA device / driver */
 DG_API int dg_set_device(int ordinal);     /* device used by subsequently created meshes */
 DG_API int dg_device_sm_count(void);
+/* Multi-GPU (one box): the DEVICE SET used by subsequently created meshes. bit i of mask = CUDA device i; the
+ * lowest set bit is the primary device. A mesh created under a set of G > 1 devices is uploaded to each of them,
+ * and every batched entry point (dg_trace_batch, dg_ep_jacobians, dg_ep_backward, dg_gfd_jacobians[_with_base],
+ * dg_batch_*) then fans a request of >= 16 384 x G elements (env DG_MULTI_MIN) out over the set: the request is cut
+ * into G contiguous shards -- of equal expected work (requested length) for host pointers, of equal counts for
+ * device pointers --, each shard runs on its device from its own host thread, and every result is written at the
+ * request index of the caller's arrays. This is the reference's fork/join site (the OpenMP loop inside trace_batch,
+ * tracer.cpp:596-603); results are bitwise independent of the set (acceptance.cpp:173-201). There is no exchange
+ * step and no reduction: all jobs of a GFD sample stay on its device. DG_MEM_DEVICE pointers live on the primary
+ * device; the other shards work on local copies moved by peer copies (NVLink P2P when the driver allows it).
+ * dg_set_device(ordinal) goes back to a single device. dg_set_device_list takes the set as an ordered list and
+ * lets an ordinal repeat (several copies on one GPU: the whole fan-out path on a one-GPU box, for tests). */
+DG_API int dg_set_devices(uint64_t mask);
+DG_API int dg_set_device_list(const int32_t* ordinals, int32_t count);
 
 /* ---- mesh ------------------------------------------------------------------------------
  * dg_mesh_derive: host-side restatement of Mesh::build (mesh.cpp:34-130). Validates the
@@ -129,7 +144,8 @@ DG_API void dg_mesh_destroy(dg_mesh* m);
 DG_API int32_t dg_mesh_face_count(const dg_mesh* m);
 DG_API int32_t dg_mesh_vertex_count(const dg_mesh* m);
 DG_API int64_t dg_mesh_device_bytes(const dg_mesh* m);
-DG_API int dg_mesh_device(const dg_mesh* m);
+DG_API int dg_mesh_device(const dg_mesh* m);            /* the primary device */
+DG_API int dg_mesh_device_count(const dg_mesh* m);      /* devices holding a copy of this mesh (>= 1) */
 
 /* ---- forward tracing ------------------------------------------------------------------- */
 typedef struct dg_trace_cfg {

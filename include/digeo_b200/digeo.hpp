@@ -195,8 +195,14 @@ class Mesh {
 
   // GPU residency: uploaded lazily by the first compute call, shared by copies of this Mesh.
   const DeviceMesh& device() const;
-  // Selects the CUDA device used by meshes uploaded afterwards (multi-GPU: one process per GPU).
+  // Selects the CUDA device used by meshes uploaded afterwards (one process per GPU).
   static void set_device(int ordinal);
+  // One process, several GPUs (dg_set_devices): meshes uploaded afterwards are replicated on every device of the
+  // mask (bit i = CUDA device i) and trace_batch / gfd_batched_many / ep_*_batch / ResidentBatch fan each large
+  // request out over them -- the GPU form of the reference's `workers` (tracer.cpp:596-603). Results stay at the
+  // request index and are bitwise independent of the set.
+  static void set_devices(std::uint64_t mask);
+  static void set_device_list(const std::vector<int>& ordinals);  // ordered; an ordinal may repeat (tests)
 
  private:
   double mean_edge_length_ = 0, total_area_ = 0;

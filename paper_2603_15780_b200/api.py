@@ -59,8 +59,12 @@ class Mesh:
     """Immutable triangle mesh: host-side derived arrays (Mesh::build, mesh.cpp:34-130) plus
     the GPU-resident fat-record store (dg_mesh_create)."""
 
-    def __init__(self, xyz, tri, device=None, upload=True, transport_cache="auto"):
+    def __init__(self, xyz, tri, device=None, upload=True, transport_cache="auto", devices=None):
+        """device: the CUDA ordinal the mesh lives on; devices: a LIST of ordinals (multi-GPU, dg_set_device_list):
+        the mesh is replicated on each of them and large batched calls fan out over the set, results at the request
+        index, bitwise independent of the set. An ordinal may repeat (several copies on one GPU, for tests)."""
         L = lib()
+        self.devices = None if devices is None else [int(x) for x in devices]
         self.transport_cache = transport_cache
         self.has_transport_cache = False
         self.uses_tma_gather = False
@@ -93,7 +97,10 @@ class Mesh:
     def upload(self, device=None):
         L = lib()
         capi.require_device()
-        if device is not None:
+        if self.devices:
+            arr = np.asarray(self.devices, np.int32)
+            check(L.dg_set_device_list(ptr(arr), len(arr)))
+        elif device is not None:
             check(L.dg_set_device(int(device)))
         h = C.c_void_p(0)
         flags = {"auto": 0, None: 0, True: 1, "on": 1, False: 2, "off": 2}[self.transport_cache]
@@ -101,6 +108,9 @@ class Mesh:
                                   ptr(self.vangle), ptr(self.vboundary), ptr(self.csr_off), ptr(self.csr_list),
                                   flags, C.addressof(h)))
         self.h = h
+        if self.devices:   # the device set is per creating thread: go back to a single device for later meshes
+            check(L.dg_set_device(self.devices[0]))
+        self.device_count = int(L.dg_mesh_device_count(h))
         self.has_transport_cache = bool(L.dg_mesh_has_transport_cache(h))
         self.uses_tma_gather = bool(L.dg_mesh_uses_tma_gather(h))
         self.gather = ("loads", "tma", "coop")[L.dg_mesh_gather_mode(h)]

@@ -34,7 +34,8 @@ STALL_MESSAGES = {
 }
 
 EXPORTS = [
-    "dg_last_error", "dg_version", "dg_device_count", "dg_set_device", "dg_device_sm_count",
+    "dg_last_error", "dg_version", "dg_device_count", "dg_set_device", "dg_set_devices", "dg_set_device_list",
+    "dg_mesh_device_count", "dg_device_sm_count",
     "dg_mesh_derive", "dg_mesh_create", "dg_mesh_create_ex", "dg_mesh_has_transport_cache", "dg_mesh_uses_tma_gather", "dg_mesh_gather_mode", "dg_mesh_destroy", "dg_mesh_face_count", "dg_mesh_vertex_count",
     "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_transition", "dg_ep_jacobians",
     "dg_ep_backward", "dg_gfd_jacobians", "dg_gfd_jacobians_with_base", "dg_trace_kernel_info",
@@ -95,6 +96,9 @@ def lib():
         for name in ("dg_mesh_face_count", "dg_mesh_vertex_count", "dg_mesh_device_bytes", "dg_mesh_device"):
             getattr(L, name).argtypes = [C.c_void_p]
         vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.dg_set_devices.argtypes = [C.c_uint64]
+        L.dg_set_device_list.argtypes = [vp, i32]
+        L.dg_mesh_device_count.argtypes = [vp]
         L.dg_mesh_derive.argtypes = [vp, i32, vp, i32] + [vp] * 11
         L.dg_mesh_create.argtypes = [vp, i32, vp, i32] + [vp] * 7
         L.dg_mesh_create_ex.argtypes = [vp, i32, vp, i32] + [vp] * 6 + [C.c_uint32, vp]

@@ -41,6 +41,15 @@ using namespace dgapi;
 namespace {
 
 thread_local int g_device = 0;
+// device set of meshes created afterwards (dg_set_devices); empty = the single device g_device. An ordinal may
+// repeat (dg_set_device_list): two copies on one GPU exercise the whole fan-out path on a one-GPU box.
+thread_local std::vector<int> g_devices;
+
+__global__ void sum_totals_kernel(const unsigned long long* parts, int count, unsigned long long* total) {
+  unsigned long long s = 0;
+  for (int i = 0; i < count; ++i) s += parts[i];
+  *total = s;
+}
 
 __global__ void build_records_kernel(const double* __restrict__ xyz, const int32_t* __restrict__ tri,
                                      const int32_t* __restrict__ adj, int32_t nf, dg::FaceRec* rec) {
@@ -131,8 +140,33 @@ int dg_set_device(int ordinal) {
   if (n == 0) return fail(DG_ERR_NO_DEVICE, "no usable CUDA device: there is no CPU fallback");
   if (ordinal < 0 || ordinal >= n) return fail(DG_ERR_INVALID_ARGS, "dg_set_device: ordinal %d out of range [0,%d)", ordinal, n);
   g_device = ordinal;
+  g_devices.clear();
   return DG_OK;
 }
+
+int dg_set_device_list(const int32_t* ordinals, int32_t count) {
+  const int n = dg_device_count();
+  if (n == 0) return fail(DG_ERR_NO_DEVICE, "no usable CUDA device: there is no CPU fallback");
+  if (!ordinals || count < 1 || count > 64) return fail(DG_ERR_INVALID_ARGS, "dg_set_device_list: 1..64 ordinals expected");
+  for (int i = 0; i < count; ++i)
+    if (ordinals[i] < 0 || ordinals[i] >= n)
+      return fail(DG_ERR_INVALID_ARGS, "dg_set_device_list: ordinal %d out of range [0,%d)", int(ordinals[i]), n);
+  g_device = ordinals[0];
+  g_devices.assign(ordinals, ordinals + count);
+  if (count == 1) g_devices.clear();
+  return DG_OK;
+}
+
+int dg_set_devices(uint64_t mask) {
+  int32_t list[64];
+  int count = 0;
+  for (int d = 0; d < 64; ++d)
+    if (mask >> d & 1) list[count++] = d;
+  if (count == 0) return fail(DG_ERR_INVALID_ARGS, "dg_set_devices: empty device mask");
+  return dg_set_device_list(list, count);
+}
+
+int dg_mesh_device_count(const dg_mesh* m) { return m ? int(m->replicas.size()) + 1 : 0; }
 
 int dg_device_sm_count(void) {
   if (dg_device_count() == 0) return 0;
@@ -355,12 +389,40 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   DG_TRY(cudaFreeAsync(d_adj, m->stream));
   DG_TRY(cudaStreamSynchronize(m->stream));
 #undef DG_TRY
+  // multi-GPU: one copy of the mesh per further device of the set (one host-to-device upload each)
+  if (g_devices.size() > 1) {
+    const std::vector<int> set = g_devices;
+    const int primary = g_device;
+    int rc = DG_OK;
+    for (size_t i = 1; i < set.size() && rc == DG_OK; ++i) {
+      g_devices.clear();
+      g_device = set[i];
+      dg_mesh* copy = nullptr;
+      rc = dg_mesh_create_ex(xyz, nv, tri, nf, adj, fnormal, vangle, vboundary, csr_off, csr_list, flags, &copy);
+      if (rc == DG_OK) {
+        m->replicas.push_back(copy);
+        if (copy->device != m->device) {   // NVLink P2P for the peer copies of device-mode requests; failure = staged copies
+          int can = 0;
+          if (cudaDeviceCanAccessPeer(&can, m->device, copy->device) == cudaSuccess && can) {
+            { DeviceGuard a(m->device); cudaDeviceEnablePeerAccess(copy->device, 0); }
+            { DeviceGuard b(copy->device); cudaDeviceEnablePeerAccess(m->device, 0); }
+            cudaGetLastError();   // "already enabled" is fine
+          }
+        }
+      }
+    }
+    g_device = primary;
+    g_devices = set;
+    if (rc != DG_OK) { dg_mesh_destroy(m); return rc; }
+  }
   *out = m;
   return DG_OK;
 }
 
 void dg_mesh_destroy(dg_mesh* m) {
   if (!m) return;
+  for (dg_mesh* copy : m->replicas) dg_mesh_destroy(copy);
+  m->replicas.clear();
   DeviceGuard guard(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   if (m->host_batch) dg_batch_destroy(m->host_batch);
@@ -575,22 +637,12 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   return DG_OK;
 }
 
-int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg,
-                   dg_trace_out* out) {
-  // whole-call contract violations, tracer.cpp:566-576
-  if (!mesh) return fail(DG_ERR_INVALID_ARGS, "trace_batch: missing mesh");
-  if (n < 0 || n > 0x7fffffffLL) return fail(DG_ERR_INVALID_ARGS, "trace_batch: batch size out of range");
-  if (!in || !out) return fail(DG_ERR_INVALID_ARGS, "trace_batch: null request or result block");
-  if (n > 0 && (!in->face || !in->bary || !in->dir))
-    return fail(DG_ERR_INVALID_ARGS, "trace_batch: starts and dirs differ in length");
-  dg_trace_cfg c{};
-  if (cfg) c = *cfg;
-  if (c.lane > DG_LANE_EXACT) return fail(DG_ERR_INVALID_ARGS, "trace_batch: unknown arithmetic lane %d", int(c.lane));
+// One device: the request runs on `mesh` (a primary without fan-out, or one device's copy).
+}  // extern "C"
+
+int dgapi::trace_batch_one(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c, dg_trace_out* out) {
   const bool device_mode = c.memory == DG_MEM_DEVICE;
   const bool record = out->poly_offsets != nullptr;
-  if (record && (!out->poly_face || !out->poly_bary || !out->poly_seg || out->poly_total < 0))
-    return fail(DG_ERR_INVALID_ARGS, "trace_batch: polyline recording needs poly_face/poly_bary/poly_seg and poly_total");
-
   DeviceGuard guard(mesh->device);
   if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
   // device mode: the caller's stream, NULL = the CUDA default stream (ordering with the caller's
@@ -618,11 +670,11 @@ int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const 
       if (mesh->host_batch) dg_batch_destroy(mesh->host_batch);
       mesh->host_batch = nullptr;
       mesh->host_batch_cap = 0;
-      int rc = dg_batch_create(mesh, n, &mesh->host_batch);
+      int rc = dgapi::batch_create_one(mesh, n, &mesh->host_batch);
       if (rc != DG_OK) return rc;
       mesh->host_batch_cap = n;
     }
-    return dg_batch_trace(mesh->host_batch, n, in, &c, out);
+    return dgapi::batch_trace_one(mesh->host_batch, n, in, &c, out);
   }
 
   Stage st(stream, device_mode);
@@ -631,6 +683,148 @@ int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const 
   cudaError_t e = st.finish();
   if (e != cudaSuccess) return fail_cuda(e, "dg_trace_batch");
   return DG_OK;
+}
+
+extern "C" {
+
+// Shard [lo, lo + m) of a request: the same pointers, offset.
+static void shard_io(const dg_trace_in* in, const dg_trace_out* out, int64_t lo, dg_trace_in* sin, dg_trace_out* so) {
+  const size_t L = size_t(lo);
+  auto at = [&](auto* p, size_t stride) { return p ? p + stride * L : p; };
+  *sin = dg_trace_in{at(in->face, 1), at(in->bary, 3), at(in->dir, 3), at(in->payload, 3)};
+  *so = dg_trace_out{};
+  so->face = at(out->face, 1); so->bary = at(out->bary, 3); so->dir = at(out->dir, 3);
+  so->traced = at(out->traced, 1); so->requested = at(out->requested, 1);
+  so->term = at(out->term, 1); so->status = at(out->status, 1); so->stall = at(out->stall, 1);
+  so->payload = at(out->payload, 3); so->transport = at(out->transport, 9);
+  so->npoints = at(out->npoints, 1); so->crossings = at(out->crossings, 1);
+}
+
+// Host-mode request on a multi-GPU mesh: contiguous shards of equal expected work, one host thread per device,
+// every shard the one-device path on its own slice of the caller's arrays (results at the request index).
+static int trace_batch_multi_host(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c,
+                                  dg_trace_out* out) {
+  const bool record = out->poly_offsets != nullptr;
+  const std::vector<Shard> shards = cut_shards(mesh, n, in->dir);
+  std::vector<uint64_t> totals(shards.size(), 0);
+  std::vector<std::vector<int64_t>> rel(shards.size());   // polyline offsets relative to the shard's first slot
+  int rc = run_shards(shards, [&](const Shard& s, int k) {
+    dg_trace_in sin;
+    dg_trace_out so;
+    shard_io(in, out, s.lo, &sin, &so);
+    so.total_crossings = out->total_crossings ? &totals[size_t(k)] : nullptr;
+    if (record) {
+      const int64_t first = out->poly_offsets[s.lo];
+      const int64_t end = s.lo + s.n < n ? out->poly_offsets[s.lo + s.n] : out->poly_total;
+      auto& r = rel[size_t(k)];
+      r.resize(size_t(s.n));
+      for (int64_t i = 0; i < s.n; ++i) r[size_t(i)] = out->poly_offsets[s.lo + i] - first;
+      so.poly_offsets = r.data();
+      so.poly_total = end - first;
+      so.poly_face = out->poly_face + first; so.poly_bary = out->poly_bary + 3 * first; so.poly_seg = out->poly_seg + first;
+    }
+    dg_trace_cfg sc = c;
+    if (s.mesh != mesh) sc.stream = nullptr;   // a caller's stream belongs to the primary device
+    return trace_batch_one(s.mesh, s.n, &sin, sc, &so);
+  });
+  if (rc != DG_OK) return rc;
+  if (out->total_crossings) {
+    uint64_t t = 0;
+    for (uint64_t v : totals) t += v;
+    *out->total_crossings = t;
+  }
+  return DG_OK;
+}
+
+// Device-mode request on a multi-GPU mesh: the caller's arrays live on the PRIMARY device and the call stays
+// asynchronous on the caller's stream. Shard 0 runs in place; every other shard runs on its device's stream after
+// an event of the caller's stream, on local copies moved by peer copies (PeerStage), and the caller's stream waits
+// for the event that follows its copy back. Equal-count shards (the weights are not on the host).
+static int trace_batch_multi_device(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c,
+                                    dg_trace_out* out) {
+  const std::vector<Shard> shards = cut_shards(mesh, n, nullptr);
+  const int S = int(shards.size());
+  cudaStream_t home = static_cast<cudaStream_t>(c.stream);
+  DeviceGuard guard(mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
+  cudaEvent_t ready = nullptr;
+  DG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  unsigned long long* parts = nullptr;
+  if (out->total_crossings) {
+    DG_CUDA(cudaMallocAsync(&parts, size_t(S) * sizeof(unsigned long long), home));
+    DG_CUDA(cudaMemsetAsync(parts, 0, size_t(S) * sizeof(unsigned long long), home));
+  }
+  DG_CUDA(cudaEventRecord(ready, home));
+  int rc = DG_OK;
+  for (int k = 0; k < S && rc == DG_OK; ++k) {
+    const Shard& s = shards[size_t(k)];
+    if (s.n == 0) continue;
+    dg_trace_in sin;
+    dg_trace_out so;
+    shard_io(in, out, s.lo, &sin, &so);
+    so.total_crossings = parts ? reinterpret_cast<uint64_t*>(parts + k) : nullptr;
+    if (s.mesh == mesh) {
+      rc = trace_batch_one(mesh, s.n, &sin, c, &so);
+      continue;
+    }
+    DeviceGuard work(s.mesh->device);
+    cudaStream_t ws = s.mesh->stream;
+    const size_t M = size_t(s.n);
+    PeerStage ps(mesh->device, s.mesh->device, ws);
+    ps.note(cudaStreamWaitEvent(ws, ready, 0));
+    dg_trace_in lin{ps.in(sin.face, M), ps.in(sin.bary, 3 * M), ps.in(sin.dir, 3 * M), ps.in(sin.payload, 3 * M)};
+    dg_trace_out lo{};
+    lo.face = ps.out(so.face, M); lo.bary = ps.out(so.bary, 3 * M); lo.dir = ps.out(so.dir, 3 * M);
+    lo.traced = ps.out(so.traced, M); lo.requested = ps.out(so.requested, M);
+    lo.term = ps.out(so.term, M); lo.status = ps.out(so.status, M); lo.stall = ps.out(so.stall, M);
+    lo.payload = ps.out(so.payload, 3 * M); lo.transport = ps.out(so.transport, 9 * M);
+    lo.npoints = ps.out(so.npoints, M); lo.crossings = ps.out(so.crossings, M);
+    lo.total_crossings = ps.out(so.total_crossings, 1);
+    if (ps.error() != cudaSuccess) { rc = fail_cuda(ps.error(), "dg_trace_batch peer staging"); break; }
+    dg_trace_cfg wc = c;
+    wc.stream = ws;
+    rc = trace_batch_one(s.mesh, s.n, &lin, wc, &lo);
+    ps.flush();
+    cudaEvent_t done = nullptr;
+    ps.note(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    if (done) {
+      ps.note(cudaEventRecord(done, ws));
+      ps.note(cudaStreamWaitEvent(home, done, 0));
+      cudaEventDestroy(done);   // released once the recorded work has completed
+    }
+    if (rc == DG_OK && ps.error() != cudaSuccess) rc = fail_cuda(ps.error(), "dg_trace_batch peer copies");
+  }
+  cudaEventDestroy(ready);
+  if (parts) {
+    if (rc == DG_OK) {
+      sum_totals_kernel<<<1, 1, 0, home>>>(parts, S, reinterpret_cast<unsigned long long*>(out->total_crossings));
+      if (cudaGetLastError() != cudaSuccess) rc = fail(DG_ERR_CUDA, "dg_trace_batch: total of the shards");
+    }
+    cudaFreeAsync(parts, home);
+  }
+  return rc;
+}
+
+int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg,
+                   dg_trace_out* out) {
+  // whole-call contract violations, tracer.cpp:566-576
+  if (!mesh) return fail(DG_ERR_INVALID_ARGS, "trace_batch: missing mesh");
+  if (n < 0 || n > 0x7fffffffLL) return fail(DG_ERR_INVALID_ARGS, "trace_batch: batch size out of range");
+  if (!in || !out) return fail(DG_ERR_INVALID_ARGS, "trace_batch: null request or result block");
+  if (n > 0 && (!in->face || !in->bary || !in->dir))
+    return fail(DG_ERR_INVALID_ARGS, "trace_batch: starts and dirs differ in length");
+  dg_trace_cfg c{};
+  if (cfg) c = *cfg;
+  if (c.lane > DG_LANE_EXACT) return fail(DG_ERR_INVALID_ARGS, "trace_batch: unknown arithmetic lane %d", int(c.lane));
+  const bool record = out->poly_offsets != nullptr;
+  if (record && (!out->poly_face || !out->poly_bary || !out->poly_seg || out->poly_total < 0))
+    return fail(DG_ERR_INVALID_ARGS, "trace_batch: polyline recording needs poly_face/poly_bary/poly_seg and poly_total");
+  // the reference's fork/join site (tracer.cpp:596-603): one request over the devices of the mesh's set
+  if (fan_out(mesh, n)) {
+    if (c.memory != DG_MEM_DEVICE) return trace_batch_multi_host(mesh, n, in, c, out);
+    if (!record) return trace_batch_multi_device(mesh, n, in, c, out);   // (device-resident polyline offsets: one device)
+  }
+  return trace_batch_one(mesh, n, in, c, out);
 }
 
 void dg_trace_kernel_info(int use_f32, int full, int* regs, int* blocks_per_sm, int* block_threads) {

@@ -29,6 +29,11 @@ struct dg_batch {
   // backward
   double *g = nullptr, *grad_v = nullptr, *grad_p = nullptr, *jv = nullptr, *jp = nullptr;
   uint8_t* degraded = nullptr;
+  // multi-GPU mesh: the resident request is cut into one shard per device; shard 0 lives in this batch, shard k in
+  // subs[k - 1] on device k (created on demand). Empty `shards` = the whole request is resident here.
+  std::vector<dgapi::Shard> shards;
+  std::vector<dg_batch*> subs;
+  int64_t n_total = 0;
 };
 
 namespace {
@@ -69,9 +74,7 @@ int64_t trace_slice_begin(int64_t n, int s, int S) {
 
 }  // namespace
 
-extern "C" {
-
-int dg_batch_create(const dg_mesh* mesh, int64_t capacity, dg_batch** out) {
+int dgapi::batch_create_one(const dg_mesh* mesh, int64_t capacity, dg_batch** out) {
   if (!out) return fail(DG_ERR_INVALID_ARGS, "dg_batch_create: null output handle");
   *out = nullptr;
   if (!mesh) return fail(DG_ERR_INVALID_ARGS, "dg_batch_create: missing mesh");
@@ -102,8 +105,14 @@ int dg_batch_create(const dg_mesh* mesh, int64_t capacity, dg_batch** out) {
   return DG_OK;
 }
 
+extern "C" {
+
+int dg_batch_create(const dg_mesh* mesh, int64_t capacity, dg_batch** out) { return batch_create_one(mesh, capacity, out); }
+
 void dg_batch_destroy(dg_batch* b) {
   if (!b) return;
+  for (dg_batch* sub : b->subs) dg_batch_destroy(sub);
+  b->subs.clear();
   DeviceGuard guard(b->device);
   for (auto& s : b->streams) if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
   cudaFree(b->face); cudaFree(b->bary); cudaFree(b->dir); cudaFree(b->o_face); cudaFree(b->o_bary); cudaFree(b->o_dir);
@@ -114,11 +123,13 @@ void dg_batch_destroy(dg_batch* b) {
   delete b;
 }
 
-int64_t dg_batch_size(const dg_batch* b) { return b && b->traced ? b->n : 0; }
+int64_t dg_batch_size(const dg_batch* b) { return b && b->traced ? (b->shards.empty() ? b->n : b->n_total) : 0; }
+
+}  // extern "C"
 
 // Forward exp map of n host-resident queries. The request is cut into slices on separate streams:
 // the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the walker of slice i.
-int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, dg_trace_out* out) {
+int dgapi::batch_trace_one(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, dg_trace_out* out) {
   if (!b) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace: missing batch");
   if (n < 0 || n > b->cap) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace: batch size exceeds the capacity");
   if (!in || !out) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace: null request or result block");
@@ -132,6 +143,7 @@ int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace
   DeviceGuard guard(b->mesh->device);
   if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
   b->traced = false;
+  b->shards.clear();
   b->n = n;
   b->traced_max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(b->mesh->nf);
   b->traced_f32 = c.use_f32 != 0;
@@ -165,7 +177,7 @@ int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace
     // One resident CTA slot per SM is left to the neighbouring slice, so that its walker ramps up
     // while this one drains (measured, 1 M geodesics: 4 slices x 4 CTAs/SM 5.8 ms, x 3 CTAs/SM 5.1 ms).
     if (S > 1 && dc.blocks_per_sm == 0) dc.blocks_per_sm = 3;
-    rc = dg_trace_batch(b->mesh, m, &din, &dc, &dout);
+    rc = trace_batch_one(b->mesh, m, &din, dc, &dout);
     if (rc != DG_OK) break;
     auto back = [&](auto* host, const auto* dev, size_t stride) {
       if (host) note(cudaMemcpyAsync(host + stride * L, dev + stride * L, M * stride * sizeof(*host), cudaMemcpyDeviceToHost, st));
@@ -193,7 +205,7 @@ int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace
 }
 
 // EP backward (diff.cpp:44-66, 328-354) on the resident samples: g in, grad_v (and grad_p) out.
-int dg_batch_ep_backward(dg_batch* b, const double* g, double* grad_v, double* grad_p, int64_t* err_index) {
+static int batch_ep_backward_one(dg_batch* b, const double* g, double* grad_v, double* grad_p, int64_t* err_index) {
   if (err_index) *err_index = -1;
   if (!b || !b->traced) return fail(DG_ERR_INVALID_ARGS, "dg_batch_ep_backward: no traced batch is resident");
   const int64_t n = b->n;
@@ -232,8 +244,8 @@ int dg_batch_ep_backward(dg_batch* b, const double* g, double* grad_v, double* g
 }
 
 // GFD backward (diff.cpp:273-326) on the resident samples.
-int dg_batch_gfd(dg_batch* b, double eps_v, double eps_p, const double* g, int32_t max_steps, double* jv, double* jp,
-                 uint8_t* degraded, double* grad_v, double* grad_p, int64_t* err_index) {
+static int batch_gfd_one(dg_batch* b, double eps_v, double eps_p, const double* g, int32_t max_steps, double* jv, double* jp,
+                         uint8_t* degraded, double* grad_v, double* grad_p, int64_t* err_index) {
   if (err_index) *err_index = -1;
   if (!b || !b->traced) return fail(DG_ERR_INVALID_ARGS, "dg_batch_gfd: no traced batch is resident");
   const int64_t n = b->n;
@@ -270,6 +282,94 @@ int dg_batch_gfd(dg_batch* b, double eps_v, double eps_p, const double* g, int32
   note(cudaStreamSynchronize(st));
   if (e != cudaSuccess) return fail_cuda(e, "dg_batch_gfd");
   return DG_OK;
+}
+
+// ---- dispatchers: a multi-GPU mesh fans the resident request out over its devices -------------------------------
+
+static dg_batch* shard_batch(dg_batch* b, int k) { return k == 0 ? b : b->subs[size_t(k) - 1]; }
+
+extern "C" {
+
+int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, dg_trace_out* out) {
+  if (!b || !in || !out || n > b->cap || !fan_out(b->mesh, n) || !in->dir || (cfg && cfg->memory != DG_MEM_HOST))
+    return batch_trace_one(b, n, in, cfg, out);
+  const std::vector<Shard> shards = cut_shards(b->mesh, n, in->dir);
+  const int S = int(shards.size());
+  b->subs.resize(size_t(S) - 1, nullptr);
+  for (int k = 1; k < S; ++k) {   // the other devices' resident batches, grown on demand
+    dg_batch*& sub = b->subs[size_t(k) - 1];
+    if (sub && sub->cap >= shards[size_t(k)].n) continue;
+    if (sub) dg_batch_destroy(sub);
+    sub = nullptr;
+    const int64_t cap = std::max<int64_t>(1, shards[size_t(k)].n + shards[size_t(k)].n / 8);
+    if (int rc = batch_create_one(shards[size_t(k)].mesh, cap, &sub)) return rc;
+  }
+  std::vector<uint64_t> totals(size_t(S), 0);
+  const size_t one = 1;
+  int rc = run_shards(shards, [&](const Shard& s, int k) {
+    const size_t L = size_t(s.lo);
+    auto at = [&](auto* p, size_t stride) { return p ? p + stride * L : p; };
+    dg_trace_in sin{in->face + L, in->bary + 3 * L, in->dir + 3 * L, nullptr};
+    dg_trace_out so = *out;
+    so.face = at(out->face, one); so.bary = at(out->bary, 3); so.dir = at(out->dir, 3);
+    so.traced = at(out->traced, one); so.requested = at(out->requested, one);
+    so.term = at(out->term, one); so.status = at(out->status, one); so.stall = at(out->stall, one);
+    so.npoints = at(out->npoints, one); so.crossings = at(out->crossings, one);
+    so.total_crossings = out->total_crossings ? &totals[size_t(k)] : nullptr;
+    return batch_trace_one(shard_batch(b, k), s.n, &sin, cfg, &so);
+  });
+  if (rc != DG_OK) { b->traced = false; return rc; }
+  if (out->total_crossings) {
+    uint64_t t = 0;
+    for (uint64_t v : totals) t += v;
+    *out->total_crossings = t;
+  }
+  b->shards = shards;
+  b->n_total = n;
+  b->traced = true;
+  return DG_OK;
+}
+
+int dg_batch_ep_backward(dg_batch* b, const double* g, double* grad_v, double* grad_p, int64_t* err_index) {
+  if (!b || b->shards.empty() || !b->traced) return batch_ep_backward_one(b, g, grad_v, grad_p, err_index);
+  if (err_index) *err_index = -1;
+  if (!g || !grad_v) return fail(DG_ERR_INVALID_ARGS, "dg_ep_backward: null argument");
+  std::vector<int64_t> idx(b->shards.size(), -1);
+  int failed = -1;
+  int rc = run_shards(b->shards, [&](const Shard& s, int k) {
+    const size_t L = size_t(s.lo);
+    return batch_ep_backward_one(shard_batch(b, k), g + 3 * L, grad_v + 3 * L, grad_p ? grad_p + 3 * L : nullptr, &idx[size_t(k)]);
+  }, &failed);
+  if (rc != DG_OK && err_index && failed >= 0 && idx[size_t(failed)] >= 0) *err_index = idx[size_t(failed)] + b->shards[size_t(failed)].lo;
+  return rc;
+}
+
+int dg_batch_gfd(dg_batch* b, double eps_v, double eps_p, const double* g, int32_t max_steps, double* jv, double* jp,
+                 uint8_t* degraded, double* grad_v, double* grad_p, int64_t* err_index) {
+  if (!b || b->shards.empty() || !b->traced)
+    return batch_gfd_one(b, eps_v, eps_p, g, max_steps, jv, jp, degraded, grad_v, grad_p, err_index);
+  if (err_index) *err_index = -1;
+  std::vector<int64_t> idx(b->shards.size(), -1);
+  std::vector<int> rcs(b->shards.size(), DG_OK);
+  std::vector<std::string> msgs(b->shards.size());
+  run_shards(b->shards, [&](const Shard& s, int k) {
+    const size_t L = size_t(s.lo);
+    auto at = [&](auto* p, size_t stride) { return p ? p + stride * L : p; };
+    rcs[size_t(k)] = batch_gfd_one(shard_batch(b, k), eps_v, eps_p, at(g, 3), max_steps, at(jv, 4), at(jp, 4), at(degraded, 4),
+                                   at(grad_v, 3), at(grad_p, 3), &idx[size_t(k)]);
+    if (rcs[size_t(k)] != DG_OK) msgs[size_t(k)] = last_error();
+    return DG_OK;
+  });
+  // whole-call failures in the reference's order (diff.cpp:273-326): the frames of every sample are built before
+  // any trace runs, so a degenerate direction anywhere wins over a failed base trace; then request order
+  int pick = -1;
+  for (int k = 0; k < int(rcs.size()); ++k)
+    if (rcs[size_t(k)] != DG_OK && (pick < 0 || (rcs[size_t(k)] == DG_ERR_DEGENERATE_DIRECTION && rcs[size_t(pick)] != DG_ERR_DEGENERATE_DIRECTION)))
+      pick = k;
+  if (pick < 0) return DG_OK;
+  last_error() = msgs[size_t(pick)];
+  if (err_index && idx[size_t(pick)] >= 0) *err_index = idx[size_t(pick)] + b->shards[size_t(pick)].lo;
+  return rcs[size_t(pick)];
 }
 
 }  // extern "C"

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <functional>
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -44,6 +45,10 @@ struct dg_mesh {
   mutable std::mutex host_batch_mu;
   mutable struct dg_batch* host_batch = nullptr;
   mutable int64_t host_batch_cap = 0;
+  // multi-GPU (dg_set_devices): copies of this mesh on the other devices of the set. Large requests are cut into
+  // contiguous shards of equal expected work, one per device, and run concurrently (dg_capi_multi.cu); results land
+  // at the request index. A replica has no replicas of its own.
+  std::vector<dg_mesh*> replicas;
   // ring of {queue_head, total_crossings} pairs so that concurrent calls never share a cursor
   static constexpr unsigned kRing = 256;
   unsigned long long* counters = nullptr;
@@ -171,6 +176,76 @@ cudaError_t ep_backward_enqueue(const dg_mesh* mesh, int64_t n, const int32_t* f
                                 const int32_t* end_face, const double* end_dir, const double* g, double* grad_v,
                                 double* grad_p, unsigned long long* err_word, cudaStream_t stream);
 int ep_error_to_rc(unsigned long long word, const char* who, int64_t* err_index);
+
+// ---- multi-GPU fan-out (dg_capi_multi.cu) ---------------------------------------------------------------
+// The reference's fork/join site is the OpenMP loop inside trace_batch (tracer.cpp:596-603); here the same call
+// fans one request out over the devices of the mesh's set. A shard is a contiguous slice [lo, lo + n) of the
+// request handled by one device's copy of the mesh.
+struct Shard { const dg_mesh* mesh; int64_t lo, n; };
+// true when a request of n elements on this mesh is to be cut (the mesh has replicas and n is large enough)
+bool fan_out(const dg_mesh* mesh, int64_t n);
+// Cuts [0, n) into one shard per device. host_dirs (3n doubles in HOST memory, or null): the requested lengths
+// are the weights, so shards have equal expected work (sampled every 64th query; cuts are multiples of 64);
+// null: equal counts.
+std::vector<Shard> cut_shards(const dg_mesh* mesh, int64_t n, const double* host_dirs);
+// Runs fn(shard, index) for every shard, shard 0 on the calling thread and the others on one host thread each;
+// returns DG_OK or the rc of the failing shard that comes first in request order (its message becomes the calling
+// thread's dg_last_error(); *first_failed receives its index).
+int run_shards(const std::vector<Shard>& shards, const std::function<int(const Shard&, int)>& fn, int* first_failed = nullptr);
+
+// Device-mode requests on a multi-GPU mesh: the caller's arrays live on the primary device; a shard that runs on
+// another device works on stream-ordered local copies, moved with peer copies (NVLink P2P when enabled) -- in()
+// copies a slice over, out() hands out a local buffer that flush() copies back into the caller's array.
+class PeerStage {
+ public:
+  PeerStage(int home_dev, int work_dev, cudaStream_t work_stream) : home_(home_dev), work_(work_dev), stream_(work_stream) {}
+  ~PeerStage() { release(); }
+  template <class T>
+  const T* in(const T* home_ptr, size_t count) {
+    if (!home_ptr || count == 0) return home_ptr;
+    void* d = alloc(count * sizeof(T));
+    if (d) note(cudaMemcpyPeerAsync(d, work_, home_ptr, home_, count * sizeof(T), stream_));
+    return static_cast<const T*>(d);
+  }
+  template <class T>
+  T* out(T* home_ptr, size_t count) {
+    if (!home_ptr || count == 0) return home_ptr;
+    void* d = alloc(count * sizeof(T));
+    if (d) backs_.push_back({d, home_ptr, count * sizeof(T)});
+    return static_cast<T*>(d);
+  }
+  void flush() {
+    for (auto& b : backs_) note(cudaMemcpyPeerAsync(b.home, home_, b.local, work_, b.bytes, stream_));
+    backs_.clear();
+    release();
+  }
+  cudaError_t error() const { return err_; }
+  void note(cudaError_t e) { if (err_ == cudaSuccess && e != cudaSuccess) err_ = e; }
+
+ private:
+  struct Back { void* local; void* home; size_t bytes; };
+  void* alloc(size_t bytes) {
+    void* d = nullptr;
+    cudaError_t e = cudaMallocAsync(&d, bytes ? bytes : 1, stream_);
+    if (e != cudaSuccess) { note(e); return nullptr; }
+    allocs_.push_back(d);
+    return d;
+  }
+  void release() {
+    for (void* d : allocs_) cudaFreeAsync(d, stream_);
+    allocs_.clear();
+  }
+  int home_, work_;
+  cudaStream_t stream_;
+  cudaError_t err_ = cudaSuccess;
+  std::vector<void*> allocs_;
+  std::vector<Back> backs_;
+};
+
+// one-device forms of the resident batch (the dg_batch_* entry points dispatch over the devices of a multi-GPU mesh)
+int trace_batch_one(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c, dg_trace_out* out);
+int batch_create_one(const dg_mesh* mesh, int64_t capacity, dg_batch** out);
+int batch_trace_one(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, dg_trace_out* out);
 
 inline int default_max_steps(int32_t nf) {  // tracer.cpp:543-545
   return int(10.0 * std::sqrt(double(nf))) + 100;

@@ -117,11 +117,60 @@ static int ep_common(const dg_mesh* mesh, int64_t n, const int32_t* face, const 
   return dgapi::ep_error_to_rc(h_err, who, err_index);
 }
 
+// A multi-GPU mesh: the samples are cut into one shard per device (host mode: equal expected work; device mode:
+// equal counts, the caller's arrays on the primary device reach the other devices through peer copies).
+static int ep_dispatch(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* v,
+                       const int32_t* end_face, const double* end_dir, const double* g, const dg_diff_cfg* cfg,
+                       double* rot, double* frames, double* grad_v, double* grad_p, int64_t* err_index,
+                       const char* who) {
+  if (!mesh || !fan_out(mesh, n) || !face || !v || !end_face || !end_dir)
+    return ep_common(mesh, n, face, v, end_face, end_dir, g, cfg, rot, frames, grad_v, grad_p, err_index, who);
+  if (err_index) *err_index = -1;
+  dg_diff_cfg c{};
+  if (cfg) c = *cfg;
+  const bool dev = c.memory == DG_MEM_DEVICE;
+  const std::vector<Shard> shards = cut_shards(mesh, n, dev ? nullptr : v);
+  cudaEvent_t ready = nullptr;
+  if (dev) {
+    DeviceGuard guard(mesh->device);
+    DG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    DG_CUDA(cudaEventRecord(ready, static_cast<cudaStream_t>(c.stream)));
+  }
+  std::vector<int64_t> idx(shards.size(), -1);
+  int failed = -1;
+  const int rc = run_shards(shards, [&](const Shard& s, int k) {
+    const size_t L = size_t(s.lo), M = size_t(s.n);
+    auto at = [&](auto* p, size_t stride) { return p ? p + stride * L : p; };
+    dg_diff_cfg sc = c;
+    if (s.mesh == mesh || !dev) {
+      if (s.mesh != mesh) sc.stream = nullptr;
+      return ep_common(s.mesh, s.n, at(face, 1), at(v, 3), at(end_face, 1), at(end_dir, 3), at(g, 3), &sc, at(rot, 9),
+                       at(frames, DG_FRAME_DOUBLES), at(grad_v, 3), at(grad_p, 3), &idx[size_t(k)], who);
+    }
+    DeviceGuard work(s.mesh->device);
+    cudaStream_t ws = s.mesh->stream;
+    PeerStage ps(mesh->device, s.mesh->device, ws);
+    ps.note(cudaStreamWaitEvent(ws, ready, 0));
+    sc.stream = ws;
+    int r = ep_common(s.mesh, s.n, ps.in(at(face, 1), M), ps.in(at(v, 3), 3 * M), ps.in(at(end_face, 1), M),
+                      ps.in(at(end_dir, 3), 3 * M), ps.in(at(g, 3), 3 * M), &sc, ps.out(at(rot, 9), 9 * M),
+                      ps.out(at(frames, DG_FRAME_DOUBLES), size_t(DG_FRAME_DOUBLES) * M), ps.out(at(grad_v, 3), 3 * M),
+                      ps.out(at(grad_p, 3), 3 * M), &idx[size_t(k)], who);
+    ps.flush();
+    ps.note(cudaStreamSynchronize(ws));   // these entry points return with the results in place (host-synchronous)
+    if (r == DG_OK && ps.error() != cudaSuccess) r = fail_cuda(ps.error(), who);
+    return r;
+  }, &failed);
+  if (ready) cudaEventDestroy(ready);
+  if (rc != DG_OK && err_index && failed >= 0 && idx[size_t(failed)] >= 0) *err_index = idx[size_t(failed)] + shards[size_t(failed)].lo;
+  return rc;
+}
+
 int dg_ep_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
                     const int32_t* end_face, const double* end_bary, const double* end_dir,
                     const dg_diff_cfg* cfg, double* rot, double* frames, int64_t* err_index) {
   (void)bary; (void)end_bary;  // origins of the frames; they do not enter the arithmetic (diff.cpp:44-66)
-  return ep_common(mesh, n, face, v, end_face, end_dir, nullptr, cfg, rot, frames, nullptr, nullptr, err_index,
+  return ep_dispatch(mesh, n, face, v, end_face, end_dir, nullptr, cfg, rot, frames, nullptr, nullptr, err_index,
                    "dg_ep_jacobians");
 }
 
@@ -129,16 +178,87 @@ int dg_ep_backward(const dg_mesh* mesh, int64_t n, const int32_t* face, const do
                    const double* end_dir, const double* g, const dg_diff_cfg* cfg, double* grad_v, double* grad_p,
                    int64_t* err_index) {
   if (n > 0 && (!g || !grad_v)) return fail(DG_ERR_INVALID_ARGS, "dg_ep_backward: null argument");
-  return ep_common(mesh, n, face, v, end_face, end_dir, g, cfg, nullptr, nullptr, grad_v, grad_p, err_index,
-                   "dg_ep_backward");
+  return ep_dispatch(mesh, n, face, v, end_face, end_dir, g, cfg, nullptr, nullptr, grad_v, grad_p, err_index,
+                     "dg_ep_backward");
+}
+
+// GFD on a multi-GPU mesh: all seven jobs of a sample stay on the sample's device (round 2 depends only on that
+// sample's round-1 results, diff.cpp:296-309), so the shards never exchange anything.
+static int gfd_dispatch(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
+                        double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
+                        uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
+                        double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* kb) {
+  if (!mesh || !fan_out(mesh, n) || !face || !bary || !v)
+    return dgapi::gfd_jacobians_impl(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
+                                     base_face, base_bary, base_dir, err_index, kb);
+  if (err_index) *err_index = -1;
+  dg_diff_cfg c{};
+  if (cfg) c = *cfg;
+  const bool dev = c.memory == DG_MEM_DEVICE;
+  const std::vector<Shard> shards = cut_shards(mesh, n, dev ? nullptr : v);
+  cudaEvent_t ready = nullptr;
+  if (dev) {
+    DeviceGuard guard(mesh->device);
+    DG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    DG_CUDA(cudaEventRecord(ready, static_cast<cudaStream_t>(c.stream)));
+  }
+  std::vector<int64_t> idx(shards.size(), -1);
+  std::vector<int> rcs(shards.size(), DG_OK);
+  std::vector<std::string> msgs(shards.size());
+  run_shards(shards, [&](const Shard& s, int k) {
+    const size_t L = size_t(s.lo), M = size_t(s.n);
+    auto at = [&](auto* p, size_t stride) { return p ? p + stride * L : p; };
+    dg_diff_cfg sc = c;
+    int r;
+    if (s.mesh == mesh || !dev) {
+      if (s.mesh != mesh) sc.stream = nullptr;
+      GfdKnownBase skb{};
+      if (kb) skb = GfdKnownBase{at(kb->face, 1), at(kb->bary, 3), at(kb->dir, 3), at(kb->term, 1), at(kb->status, 1)};
+      r = dgapi::gfd_jacobians_impl(s.mesh, s.n, at(face, 1), at(bary, 3), at(v, 3), eps_v, eps_p, at(g, 3), &sc, at(jv, 4),
+                                    at(jp, 4), at(degraded, 4), at(frames, DG_FRAME_DOUBLES), at(grad_v, 3), at(grad_p, 3),
+                                    at(base_face, 1), at(base_bary, 3), at(base_dir, 3), &idx[size_t(k)], kb ? &skb : nullptr);
+    } else {
+      DeviceGuard work(s.mesh->device);
+      cudaStream_t ws = s.mesh->stream;
+      PeerStage ps(mesh->device, s.mesh->device, ws);
+      ps.note(cudaStreamWaitEvent(ws, ready, 0));
+      sc.stream = ws;
+      GfdKnownBase skb{};
+      if (kb) skb = GfdKnownBase{ps.in(at(kb->face, 1), M), ps.in(at(kb->bary, 3), 3 * M), ps.in(at(kb->dir, 3), 3 * M),
+                                 ps.in(at(kb->term, 1), M), ps.in(at(kb->status, 1), M)};
+      r = dgapi::gfd_jacobians_impl(s.mesh, s.n, ps.in(at(face, 1), M), ps.in(at(bary, 3), 3 * M), ps.in(at(v, 3), 3 * M), eps_v,
+                                    eps_p, ps.in(at(g, 3), 3 * M), &sc, ps.out(at(jv, 4), 4 * M), ps.out(at(jp, 4), 4 * M),
+                                    ps.out(at(degraded, 4), 4 * M), ps.out(at(frames, DG_FRAME_DOUBLES), size_t(DG_FRAME_DOUBLES) * M),
+                                    ps.out(at(grad_v, 3), 3 * M), ps.out(at(grad_p, 3), 3 * M), ps.out(at(base_face, 1), M),
+                                    ps.out(at(base_bary, 3), 3 * M), ps.out(at(base_dir, 3), 3 * M), &idx[size_t(k)],
+                                    kb ? &skb : nullptr);
+      ps.flush();
+      ps.note(cudaStreamSynchronize(ws));
+      if (r == DG_OK && ps.error() != cudaSuccess) r = fail_cuda(ps.error(), "dg_gfd_jacobians peer copies");
+    }
+    rcs[size_t(k)] = r;
+    if (r != DG_OK) msgs[size_t(k)] = last_error();
+    return DG_OK;
+  });
+  if (ready) cudaEventDestroy(ready);
+  // whole-call failures in the reference's order (diff.cpp:273-326): every sample's frames are built before any
+  // trace runs, so a degenerate direction anywhere wins over a failed base trace; then request order
+  int pick = -1;
+  for (int k = 0; k < int(rcs.size()); ++k)
+    if (rcs[size_t(k)] != DG_OK && (pick < 0 || (rcs[size_t(k)] == DG_ERR_DEGENERATE_DIRECTION && rcs[size_t(pick)] != DG_ERR_DEGENERATE_DIRECTION)))
+      pick = k;
+  if (pick < 0) return DG_OK;
+  last_error() = msgs[size_t(pick)];
+  if (err_index && idx[size_t(pick)] >= 0) *err_index = idx[size_t(pick)] + shards[size_t(pick)].lo;
+  return rcs[size_t(pick)];
 }
 
 int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
                      double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
                      uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
                      double* base_bary, double* base_dir, int64_t* err_index) {
-  return dgapi::gfd_jacobians_impl(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
-                                   base_face, base_bary, base_dir, err_index, nullptr);
+  return gfd_dispatch(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
+                      base_face, base_bary, base_dir, err_index, nullptr);
 }
 
 int dg_gfd_jacobians_with_base(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
@@ -149,8 +269,8 @@ int dg_gfd_jacobians_with_base(const dg_mesh* mesh, int64_t n, const int32_t* fa
   if (n > 0 && (!base_face || !base_bary || !base_dir || !base_term || !base_status))
     return fail(DG_ERR_INVALID_ARGS, "dg_gfd_jacobians_with_base: null base trace array");
   const GfdKnownBase kb{base_face, base_bary, base_dir, base_term, base_status};
-  return dgapi::gfd_jacobians_impl(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
-                                   nullptr, nullptr, nullptr, err_index, &kb);
+  return gfd_dispatch(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
+                      nullptr, nullptr, nullptr, err_index, &kb);
 }
 
 }  // extern "C"

@@ -138,6 +138,11 @@ std::span<const int> Mesh::vertex_faces(int v) const {
 }
 
 void Mesh::set_device(int ordinal) { check(dg_set_device(ordinal)); }
+void Mesh::set_devices(std::uint64_t mask) { check(dg_set_devices(mask)); }
+void Mesh::set_device_list(const std::vector<int>& ordinals) {
+  std::vector<int32_t> list(ordinals.begin(), ordinals.end());
+  check(dg_set_device_list(list.data(), int32_t(list.size())));
+}
 
 const DeviceMesh& Mesh::device() const {
   if (!device_) {

@@ -302,9 +302,58 @@ static void test_differentials() {
   CHECK(near(pp.grad_v, {.3, -.2, 0}, 1e-6) && near(pp.grad_p, {.3, -.2, 0}, 1e-6));
 }
 
+// acceptance.cpp:173-201 with devices in the place of workers: the same request on one copy of the mesh and
+// fanned out over a device set (two and three copies on GPU 0 -- the whole fork/join path on a one-GPU box)
+// gives bit-identical traces, polylines included, and identical GFD Jacobians.
+static void test_device_set_is_bitwise_invisible() {
+  auto request = [](const Mesh& m, int n, bool polyline) {
+    BatchRequest req;
+    req.mesh = &m;
+    req.config.record_polyline = polyline;
+    unsigned s = 777;
+    auto rnd = [&] { s = s * 1664525u + 1013904223u; return double(s >> 8) / double(1u << 24); };
+    for (int i = 0; i < n; ++i) {
+      int f = int(rnd() * m.face_count()) % m.face_count();
+      double r1 = std::sqrt(rnd()), r2 = rnd();
+      SurfacePoint p{f, {1 - r1, r1 * (1 - r2), r1 * r2}};
+      const auto& c = m.faces[f];
+      Vec3d e1 = normalized(m.vertices[c[1]] - m.vertices[c[0]]);
+      Vec3d e2 = cross(m.face_normals[f], e1);
+      double phi = 2 * M_PI * rnd();
+      req.starts.push_back(p);
+      req.dirs.push_back({p, (e1 * std::cos(phi) + e2 * std::sin(phi)) * (0.05 + 0.6 * rnd() * rnd())});
+    }
+    return req;
+  };
+  const int n = 52000;
+  Mesh::set_device(0);
+  Mesh one = icosphere(3);
+  BatchRequest r1 = request(one, n, true);
+  auto base = trace_batch(r1);
+  std::vector<GfdSample> samples;
+  for (int i = 0; i < n; ++i) samples.push_back({r1.starts[i], r1.dirs[i].dir});
+  auto jac1 = gfd_batched_many(one, samples, default_gfd_config(one));
+  for (int copies = 2; copies <= 3; ++copies) {
+    Mesh::set_device_list(std::vector<int>(size_t(copies), 0));
+    Mesh many = icosphere(3);
+    BatchRequest r2 = request(many, n, true);
+    auto fan = trace_batch(r2);
+    int differ = 0;
+    for (int i = 0; i < n; ++i) differ += traces_bit_equal(base[i], fan[i]) ? 0 : 1;
+    CHECK(differ == 0);
+    auto jac2 = gfd_batched_many(many, samples, default_gfd_config(many));
+    int jdiff = 0;
+    for (int i = 0; i < n; ++i)
+      jdiff += ((jac1[i].j_v - jac2[i].j_v).max_abs() == 0 && (jac1[i].j_p - jac2[i].j_p).max_abs() == 0) ? 0 : 1;
+    CHECK(jdiff == 0);
+  }
+  Mesh::set_device(0);
+}
+
 int main() {
   try {
     test_mesh();
+    test_device_set_is_bitwise_invisible();
     test_square_known_answers();
     test_sphere_batch_and_transport();
     test_single_transitions();
