@@ -10,6 +10,7 @@
  *   dg_mesh_create        <- (device mirror of) class Mesh     proj/include/digeo/mesh.hpp:40-83
  *   dg_trace_batch        <- trace_batch / trace_batch_serial  proj/src/tracer.cpp:596-610
  *                            (OpenMP loop at :600 over run_one :578 -> Kernel<S>::run :490)
+ *   dg_trace_polylines    <- trace_batch with record_polyline  proj/src/tracer.cpp:84-89,596-603
  *   dg_transition         <- geodesic_step, transport_over_edge, transport_over_vertex,
  *                            boundary_continue                 proj/src/tracer.cpp:630-735
  *   dg_ep_jacobians       <- ep_jacobians (+ frames)           proj/src/diff.cpp:13-66
@@ -205,6 +206,25 @@ typedef struct dg_trace_out {
 
 DG_API int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in,
                           const dg_trace_cfg* cfg, dg_trace_out* out);
+
+/* trace_batch with the reference's DEFAULT TraceConfig, record_polyline = true (tracer.hpp:22), in ONE call: the
+ * library records, sizes, compacts and copies on the device (capped first pass, device scan, compaction, a second pass
+ * for the few traces that outgrew their slots) -- no host-side scan, no second call. out: as dg_trace_batch with the
+ * poly_* fields NULL (npoints is filled when asked for). *poly receives the polylines in PINNED HOST arrays owned by
+ * the mesh: offsets[n + 1] (exclusive scan of the point counts; offsets[n] = total), face[total], bary[3 total],
+ * seg[total] (length of the segment ENDING at a point, 0 at a start point). They stay valid until the next
+ * dg_trace_polylines call on this mesh or its destruction: copy what must live longer. Host pointers only
+ * (cfg->memory = DG_MEM_HOST, cfg->stream = NULL); runs on the mesh's primary device. Same bits as the two-call
+ * form (dg_trace_batch sized by npoints, then with poly_offsets). */
+typedef struct dg_polylines {
+  int64_t total;
+  const int64_t* offsets;
+  const int32_t* face;
+  const double* bary;
+  const double* seg;
+} dg_polylines;
+DG_API int dg_trace_polylines(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg,
+                              dg_trace_out* out, dg_polylines* poly);
 
 /* Registers per thread, resident CTAs per SM and CTA size of a tracer kernel variant.
  * full: bit 2 = the TMA-gather variant of the fast walker, bit 3 = its cooperative-loads variant,

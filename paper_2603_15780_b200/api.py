@@ -146,9 +146,12 @@ class Mesh:
     # ------------------------------------------------------------------ forward tracing
     def trace_batch(self, face, bary, dirs, payload=None, max_steps=0, hole_avoidance=False, want_q=False,
                     record_polyline=False, use_f32=False, sort_by_face=False, refill_min=0, blocks_per_sm=0,
-                    out=None, generic_walker=False, walker="auto"):
+                    out=None, generic_walker=False, walker="auto", two_call_polylines=False, poly_views=False):
         """trace_batch (tracer.cpp:596) on host arrays; results at the request index. `out`: a
-        TraceResult of a previous call of the same size whose (e.g. pinned) arrays are reused."""
+        TraceResult of a previous call of the same size whose (e.g. pinned) arrays are reused.
+        record_polyline: ONE call (dg_trace_polylines: capped first pass, device scan, compaction); the polylines
+        are copied out of the mesh's pinned arrays unless poly_views=True (views: valid until the next recording
+        call on this mesh). two_call_polylines=True runs the count call + host scan + fill call instead."""
         h = self._handle()
         face, bary, dirs, payload = _i32(face), _f64(bary), _f64(dirs), _f64(payload)
         n = len(face)
@@ -179,6 +182,23 @@ class Mesh:
                            C.addressof(total), ptr(off), tot, ptr(pf), ptr(pb), ptr(ps))
             check(lib().dg_trace_batch(h, n, C.addressof(tin), C.addressof(cfg), C.addressof(out)))
 
+        if record_polyline and not two_call_polylines and not sort_by_face:
+            out_s = TraceOut(ptr(r.face), ptr(r.bary), ptr(r.dir), ptr(r.traced), ptr(r.requested), ptr(r.term),
+                             ptr(r.status), ptr(r.stall), ptr(r.payload), ptr(r.q), ptr(r.npoints), ptr(r.crossings),
+                             C.addressof(total), None, 0, None, None, None)
+            pl = capi.Polylines()
+            check(lib().dg_trace_polylines(h, n, C.addressof(tin), C.addressof(cfg), C.addressof(out_s), C.addressof(pl)))
+            tot = int(pl.total)
+            view = lambda p, count, shape: (np.ctypeslib.as_array(p, shape=(count,)).reshape(shape) if count else
+                                            np.empty(shape, np.ctypeslib.as_array(p, shape=(1,)).dtype if p else np.float64))
+            keep = (lambda a: a) if poly_views else (lambda a: a.copy())
+            r.poly_offsets = keep(np.ctypeslib.as_array(pl.offsets, shape=(n + 1,)))
+            r.poly_face = keep(view(pl.face, tot, (tot,))) if tot else np.empty(0, np.int32)
+            r.poly_bary = keep(view(pl.bary, 3 * tot, (tot, 3))) if tot else np.empty((0, 3))
+            r.poly_seg = keep(view(pl.seg, tot, (tot,))) if tot else np.empty(0)
+            r.total_crossings = int(total.value)
+            r.errors = [(int(i), capi.STALL_MESSAGES[int(r.stall[i])]) for i in np.nonzero(r.status)[0]]
+            return r
         call(None, None, None, None, 0)
         if record_polyline:
             # two passes: the first sized the polylines (npoints), the second writes them

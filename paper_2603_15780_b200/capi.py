@@ -37,7 +37,7 @@ EXPORTS = [
     "dg_last_error", "dg_version", "dg_device_count", "dg_set_device", "dg_set_devices", "dg_set_device_list",
     "dg_mesh_device_count", "dg_device_sm_count",
     "dg_mesh_derive", "dg_mesh_create", "dg_mesh_create_ex", "dg_mesh_has_transport_cache", "dg_mesh_uses_tma_gather", "dg_mesh_gather_mode", "dg_mesh_destroy", "dg_mesh_face_count", "dg_mesh_vertex_count",
-    "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_transition", "dg_ep_jacobians",
+    "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_trace_polylines", "dg_transition", "dg_ep_jacobians",
     "dg_ep_backward", "dg_gfd_jacobians", "dg_gfd_jacobians_with_base", "dg_trace_kernel_info",
     "dg_batch_create", "dg_batch_destroy", "dg_batch_size", "dg_batch_trace", "dg_batch_ep_backward", "dg_batch_gfd",
 ]
@@ -70,6 +70,11 @@ class TraceOut(C.Structure):
                 ("crossings", C.c_void_p), ("total_crossings", C.c_void_p), ("poly_offsets", C.c_void_p),
                 ("poly_total", C.c_int64), ("poly_face", C.c_void_p), ("poly_bary", C.c_void_p),
                 ("poly_seg", C.c_void_p)]
+
+
+class Polylines(C.Structure):
+    _fields_ = [("total", C.c_int64), ("offsets", C.POINTER(C.c_int64)), ("face", C.POINTER(C.c_int32)),
+                ("bary", C.POINTER(C.c_double)), ("seg", C.POINTER(C.c_double))]
 
 
 class DiffCfg(C.Structure):
@@ -106,6 +111,7 @@ def lib():
         L.dg_mesh_uses_tma_gather.argtypes = [vp]
         L.dg_mesh_gather_mode.argtypes = [vp]
         L.dg_trace_batch.argtypes = [vp, i64, vp, vp, vp]
+        L.dg_trace_polylines.argtypes = [vp, i64, vp, vp, vp, vp]
         L.dg_transition.argtypes = [vp, C.c_int, i64, vp, vp, vp, vp, C.c_int] + [vp] * 8
         L.dg_ep_jacobians.argtypes = [vp, i64] + [vp] * 10
         L.dg_ep_backward.argtypes = [vp, i64] + [vp] * 9

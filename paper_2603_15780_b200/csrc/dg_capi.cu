@@ -426,6 +426,7 @@ void dg_mesh_destroy(dg_mesh* m) {
   DeviceGuard guard(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   if (m->host_batch) dg_batch_destroy(m->host_batch);
+  poly_store_free(m->poly);
   if (m->small_pin) cudaFreeHost(m->small_pin);
   cudaFree(m->small_dev);
   cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);

@@ -18,6 +18,7 @@
 #include "dg_kernels.cuh"
 
 struct dg_batch;
+struct dg_poly_store;
 
 struct dg_mesh {
   int device = 0;
@@ -45,6 +46,9 @@ struct dg_mesh {
   mutable std::mutex host_batch_mu;
   mutable struct dg_batch* host_batch = nullptr;
   mutable int64_t host_batch_cap = 0;
+  // one-call polyline recording (dg_capi_poly.cu): pinned host arrays handed to the caller, reused across calls
+  mutable std::mutex poly_mu;
+  mutable dg_poly_store* poly = nullptr;
   // multi-GPU (dg_set_devices): copies of this mesh on the other devices of the set. Large requests are cut into
   // contiguous shards of equal expected work, one per device, and run concurrently (dg_capi_multi.cu); results land
   // at the request index. A replica has no replicas of its own.
@@ -242,6 +246,7 @@ class PeerStage {
   std::vector<Back> backs_;
 };
 
+void poly_store_free(dg_poly_store* s);
 // one-device forms of the resident batch (the dg_batch_* entry points dispatch over the devices of a multi-GPU mesh)
 int trace_batch_one(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c, dg_trace_out* out);
 int batch_create_one(const dg_mesh* mesh, int64_t capacity, dg_batch** out);

@@ -34,7 +34,9 @@ struct TraceParams {
   double* o_transport;
   int32_t* o_npoints;
   int32_t* o_crossings;
-  const int64_t* poly_offsets;  // non-null: record polylines
+  const int64_t* poly_offsets;  // non-null: record polylines, trace q from slot poly_offsets[q]
+  int32_t poly_cap;             // > 0 (poly_offsets null): record polylines, trace q owns slots [q cap, (q + 1) cap);
+                                // points beyond are counted in o_npoints but not written (dg_trace_polylines, pass 1)
   int32_t* poly_face;
   double* poly_bary;
   double* poly_seg;

@@ -106,9 +106,10 @@ __global__ void __launch_bounds__(kBlockThreads, kFull ? DG_TRACE_MIN_BLOCKS_FUL
               has_pay = norm2(pay) > 0.0;  // tracer.cpp:582
             }
             T.reset();
-            if (kFull && p.poly_offsets) {
+            if (kFull && (p.poly_offsets || p.poly_cap > 0)) {
               T.sink.face = p.poly_face; T.sink.bary = p.poly_bary; T.sink.seg = p.poly_seg;
-              T.sink.base = p.poly_offsets[q];
+              T.sink.base = p.poly_offsets ? p.poly_offsets[q] : int64_t(q) * p.poly_cap;
+              T.sink.cap = p.poly_cap;
             }
             live = T.initialise(f, b, v, pay, has_pay, p.want_q != 0);
             if (!live) write_result<S, kFull, kCached>(p, q, T);
@@ -247,7 +248,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   // a payload to transport, hole avoidance, a polyline to record -- anything but the transport matrix:
   // the fast walker carries the payload along, writes one polyline point per step and leaves boundary
   // events to the full Tracer behind it
-  const bool payload_only = (p.payload || p.o_payload || p.hole_avoidance || p.poly_offsets) && !p.want_q && !p.o_transport;
+  const bool payload_only = (p.payload || p.o_payload || p.hole_avoidance || p.poly_offsets || p.poly_cap > 0) && !p.want_q && !p.o_transport;
   if (payload_only && shape.walker != 1 && fast_walk_enabled()) return fast(std::integral_constant<int, 1>{});
   // the transport matrix as well: three more vectors through every fold isometry
   if (p.want_q && shape.walker != 1 && fast_walk_enabled()) return fast(std::integral_constant<int, 2>{});

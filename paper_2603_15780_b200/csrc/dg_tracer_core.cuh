@@ -56,12 +56,15 @@ template <class S> struct AxisRotate {  // tracer.cpp:301
   DG_HD V3<S> operator()(const V3<S>& w) const { return rotate_about(w, axis, angle); }
 };
 
-// Optional polyline sink: slot j of this trace lives at base + j.
+// Optional polyline sink: slot j of this trace lives at base + j. cap > 0: the trace owns `cap` slots only (the
+// capped first pass of one-call recording, dg_trace_polylines); points beyond them are counted, not written.
 struct PolySink {
   int32_t* face;
   double* bary;
   double* seg;
   int64_t base;  // < 0: not recording
+  int32_t cap;   // 0: unbounded
+  DG_HD bool room(int npoints) const { return cap == 0 || npoints < cap; }
 };
 
 // kFull = payload / transport-matrix / hole-avoidance / polyline support compiled in. The lite
@@ -104,7 +107,7 @@ struct Tracer {
     traced = 0.0;
     npoints = crossings = steps = 0;
     status = kStatusOk; stall_code = kStallNone; term = kTermLength; last_event = kEvAdvanced;
-    sink.base = -1;
+    sink.base = -1; sink.cap = 0;
   }
 
   DG_HD void set_face(int f) { face = f; cur = load_face<S>(m, f); }
@@ -120,7 +123,7 @@ struct Tracer {
   // tracer.cpp:84-89
   DG_HD void push_point(S seg_len) {
     traced += double(seg_len);
-    if (kFull && sink.base >= 0) {
+    if (kFull && sink.base >= 0 && sink.room(npoints)) {
       V3<double> b = widened_bary();
       int64_t o = sink.base + npoints;
       sink.face[o] = face;
@@ -130,7 +133,7 @@ struct Tracer {
     ++npoints;
   }
   DG_HD void push_start() {
-    if (kFull && sink.base >= 0) {
+    if (kFull && sink.base >= 0 && sink.room(npoints)) {
       V3<double> b = widened_bary();
       int64_t o = sink.base + npoints;
       sink.face[o] = face;

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <limits>
+#include <mutex>
 #include <cstdlib>
 #include <fstream>
 #include <sstream>
@@ -79,9 +80,13 @@ class DeviceMesh {
   DeviceMesh(const DeviceMesh&) = delete;
   DeviceMesh& operator=(const DeviceMesh&) = delete;
   const dg_mesh* handle() const { return h_; }
+  // serialises polyline-recording calls on this mesh: their polylines live in arrays the mesh hands out until
+  // its next recording call (dg_trace_polylines), and trace_batch must stay re-entrant
+  std::mutex& polyline_mutex() const { return poly_mu_; }
 
  private:
   dg_mesh* h_;
+  mutable std::mutex poly_mu_;
 };
 
 namespace {
@@ -320,21 +325,16 @@ std::vector<GeodesicTrace> run_batch(const Mesh& m, const std::vector<int32_t>& 
   o.payload = any_payload ? pay.data() : nullptr;
   o.transport = cfg.want_transport_matrix ? q.data() : nullptr;
   o.npoints = np.data();
-  check(dg_trace_batch(h, int64_t(n), &in, &k, &o));
-
-  std::vector<int64_t> off;
-  std::vector<int32_t> pf;
-  std::vector<double> pb, ps;
-  if (cfg.record_polyline) {  // second pass writes the polylines sized by the first
-    off.resize(n);
-    int64_t total = 0;
-    for (size_t i = 0; i < n; ++i) { off[i] = total; total += np[i]; }
-    pf.resize(size_t(total)); pb.resize(3 * size_t(total)); ps.resize(size_t(total));
-    dg_trace_out o2{};
-    o2.poly_offsets = off.data(); o2.poly_total = total;
-    o2.poly_face = pf.data(); o2.poly_bary = pb.data(); o2.poly_seg = ps.data();
-    if (total > 0) check(dg_trace_batch(h, int64_t(n), &in, &k, &o2));
-  }
+  // record_polyline (the reference's default): one call -- the device sizes, compacts and copies the polylines
+  // (dg_trace_polylines); they are read straight out of the mesh's pinned arrays below
+  dg_polylines pl{};
+  std::unique_lock<std::mutex> poly_lock(m.device().polyline_mutex(), std::defer_lock);
+  if (cfg.record_polyline) poly_lock.lock();
+  if (cfg.record_polyline) check(dg_trace_polylines(h, int64_t(n), &in, &k, &o, &pl));
+  else check(dg_trace_batch(h, int64_t(n), &in, &k, &o));
+  const int64_t* off = pl.offsets;
+  const int32_t* pf = pl.face;
+  const double *pb = pl.bary, *ps = pl.seg;
   for (size_t i = 0; i < n; ++i) {
     GeodesicTrace& t = out[i];
     t.final_point = SurfacePoint{of[i], get3(ob.data(), i)};
@@ -360,7 +360,7 @@ std::vector<GeodesicTrace> run_batch(const Mesh& m, const std::vector<int32_t>& 
       t.segment_lengths.resize(np[i] - 1);
       for (int j = 0; j < np[i]; ++j) {
         const size_t s = size_t(off[i]) + j;
-        t.points[j] = SurfacePoint{pf[s], get3(pb.data(), s)};
+        t.points[j] = SurfacePoint{pf[s], get3(pb, s)};
         if (j > 0) t.segment_lengths[j - 1] = ps[s];
       }
     }

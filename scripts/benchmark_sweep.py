@@ -21,7 +21,8 @@ def run(rm, name, batch, section):
     f, b, d = rm.sample_queries(42, batch, 0.1, np.pi / 2)
     backends = {"serial": lambda: rm.trace_batch(f, b, d, record_polyline=True, workers=-1),
                 "parallel": lambda: rm.trace_batch(f, b, d, record_polyline=True, workers=0),
-                "gpu": lambda: m.trace_batch(f, b, d, record_polyline=True),
+                "gpu": lambda: m.trace_batch(f, b, d, record_polyline=True, poly_views=True),   # one call, dg_trace_polylines
+                "gpu_two_call": lambda: m.trace_batch(f, b, d, record_polyline=True, two_call_polylines=True),
                 "gpu_nopolyline": lambda: m.trace_batch(f, b, d)}
     for backend, fn in backends.items():
         fn()

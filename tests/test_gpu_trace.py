@@ -306,3 +306,39 @@ def test_transport_cache_is_bit_identical(gpu, ref):
             for k in ("face", "bary", "dir", "traced", "term", "status", "npoints", "crossings", "poly_face",
                       "poly_bary", "poly_seg") + (("payload", "q") if kw else ()):
                 assert np.array_equal(getattr(x, k), getattr(y, k)), k
+
+
+def test_one_call_polylines_give_the_bits_of_the_two_call_form(gpu, ref):
+    """dg_trace_polylines (capped first pass, device scan, compaction, second pass for the traces that outgrew
+    their slots) against the count call + host scan + fill call, and against the reference: every polyline bit.
+    Covers: slots that always suffice (small batch), a slot budget so tight that most traces need pass 2, payload +
+    transport matrix + hole avoidance on an open mesh, rejected starts and zero-length requests (0 / 1 points)."""
+    import os
+    rm = ref.RefMesh.icosphere(4)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(5, 30000, 0.02, 3.0)
+    f[7] = -1
+    d[11] = 0.0
+    for count in (1, 60, 30000):
+        a = m.trace_batch(f[:count], b[:count], d[:count], record_polyline=True)
+        t = m.trace_batch(f[:count], b[:count], d[:count], record_polyline=True, two_call_polylines=True)
+        r = rm.trace_batch(f[:count], b[:count], d[:count], record_polyline=True)
+        for k in ("npoints", "poly_face", "poly_bary", "poly_seg", "face", "bary", "dir", "traced", "crossings"):
+            assert np.array_equal(getattr(a, k), getattr(t, k)), (count, k)
+        assert np.array_equal(a.poly_offsets, np.concatenate([[0], np.cumsum(a.npoints)]))
+        assert_trace_equal(r, a, count)
+        assert a.total_crossings == t.total_crossings
+    # pass 2 for most traces: 16 points of slot per trace at this batch size
+    os.environ["DG_POLY_SLOT_BUDGET"] = "1024"
+    pm = ref.RefMesh.plane(14, 11, 1.0, 3)
+    mp = gpu_mesh(gpu, pm)
+    f, b, d = pm.sample_queries(6, 20000, 0.05, 2.5)
+    pay = np.random.default_rng(3).normal(size=(len(f), 3))
+    kw = dict(payload=pay, want_q=True, hole_avoidance=True)
+    a = mp.trace_batch(f, b, d, record_polyline=True, **kw)
+    t = mp.trace_batch(f, b, d, record_polyline=True, two_call_polylines=True, **kw)
+    r = pm.trace_batch(f, b, d, record_polyline=True, **kw)
+    for k in ("npoints", "poly_face", "poly_bary", "poly_seg", "payload", "q"):
+        assert np.array_equal(getattr(a, k), getattr(t, k)), k
+    assert_trace_equal(r, a, len(f), payload=True, q=True)
+    del os.environ["DG_POLY_SLOT_BUDGET"]
