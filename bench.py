@@ -384,9 +384,23 @@ def measure(key, args, ctx, headline):
     ev = lambda: torch.cuda.Event(enable_timing=True)
     trace_ms = []
 
-    def step(timed):
+    def step(timed, fused=True):
         """forward + backward with everything resident in HBM; returns the number of our kernels launched."""
         e0, e1 = ev(), ev()
+        if scheme == "gfd" and fused:
+            # the forward of a GFD step IS GFD's base trace (diff.cpp:288-294): it rides in round 2 as the fourth
+            # sibling of the sample's re-traces (dg_trace_gfd); the backward is the pull-back of g (dg_gfd_pullback)
+            e0.record()
+            mesh.trace_gfd_device(F, B, D, o, eps, eps, blk.col["jv"], blk.col["jp"])
+            e1.record()
+            mesh.gfd_pullback_device(F, D, o["face"], blk.col["jv"], blk.col["jp"], G, blk.col["grad_v"], blk.col["grad_p"])
+            launches = 2 + 2 + 3 + 1   # round 1 (job builder, seeds walker), round 2 (job builder, 4-sibling walker),
+            #                            par jobs (builder, walker), assemble; pull-back
+            if world > 1:
+                gather()
+            if timed:
+                trace_ms.append((e0, e1))
+            return launches
         e0.record()
         mesh.trace_batch_device(F, B, D, o, max_steps=max_steps)
         e1.record()
@@ -399,16 +413,19 @@ def measure(key, args, ctx, headline):
             mesh.gfd_device(F, B, D, eps, eps, G, blk.col["jv"], blk.col["jp"], blk.col["grad_v"], blk.col["grad_p"], base=o)
             launches += 2 + 3   # round 1 (job builder, payload walker on the seeds) + round 2 (job builder, walker on
             #                     the sibling groups, assemble); DESIGN.md 3.3
-        if world > 1:   # results of all shards gathered over NVLink: one collective of the SoA block, no reduction
-            if ctx["backend"] == "nccl":
-                dist.all_gather_into_tensor(gathered, blk.buf)
-            else:       # functional test of the N>1 path on CPU-side collectives (gloo)
-                parts = [torch.empty(blk.nbytes, dtype=torch.uint8) for _ in range(world)]
-                dist.all_gather(parts, blk.buf.cpu())
-                gathered.copy_(torch.cat(parts))
+        if world > 1:
+            gather()
         if timed:
             trace_ms.append((e0, e1))
         return launches
+
+    def gather():   # results of all shards gathered over NVLink: one collective of the SoA block, no reduction
+        if ctx["backend"] == "nccl":
+            dist.all_gather_into_tensor(gathered, blk.buf)
+        else:       # functional test of the N>1 path on CPU-side collectives (gloo)
+            parts = [torch.empty(blk.nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, blk.buf.cpu())
+            gathered.copy_(torch.cat(parts))
 
     def sync_all():
         if world > 1:
@@ -434,6 +451,24 @@ def measure(key, args, ctx, headline):
         sync_all()
     step_ms = [s.elapsed_time(e) for s, e in marks]
     tr_ms = [s.elapsed_time(e) for s, e in trace_ms]
+    separate = None
+    if scheme == "gfd":
+        # for comparison: the same step as two separate calls -- a lone forward launch, then GFD with the forward
+        # results as known base (three sibling re-traces per sample)
+        trace_ms.clear()
+        sep_marks = []
+        step(False, fused=False)
+        sync_all()
+        for _ in range(steps):
+            flush.fill_(1)
+            s, e = ev(), ev()
+            s.record()
+            step(True, fused=False)
+            e.record()
+            sep_marks.append((s, e))
+        sync_all()
+        separate = {"ms_per_step": float(np.mean([s.elapsed_time(e) for s, e in sep_marks])),
+                    "forward_ms": float(np.mean([s.elapsed_time(e) for s, e in trace_ms]))}
 
     def over_ranks(x, op):
         v = torch.tensor([float(x)], dtype=torch.float64, device=dev)
@@ -463,7 +498,7 @@ def measure(key, args, ctx, headline):
     batch = dg.Batch(mesh, n)
 
     def e2e_step():
-        batch.trace(hf, hb, hd, out=res, max_steps=max_steps)
+        batch.trace(hf, hb, hd, out=res, max_steps=max_steps, gfd=(scheme == "gfd"))
         if scheme == "ep":
             batch.ep_backward(hg, grad_v=hgv)
         elif scheme == "gfd":
@@ -488,7 +523,7 @@ def measure(key, args, ctx, headline):
                           status=res.status, stall=None, npoints=None, crossings=None)
 
     def e2e_lean():
-        batch.trace(hf, hb, hd, out=lean, max_steps=max_steps)
+        batch.trace(hf, hb, hd, out=lean, max_steps=max_steps, gfd=(scheme == "gfd"))
         if scheme == "ep":
             batch.ep_backward(hg, grad_v=hgv)
         elif scheme == "gfd":
@@ -503,6 +538,9 @@ def measure(key, args, ctx, headline):
         return None
     peak, peak_src = measured_peak()
     t_trace = float(np.mean(tr_ms)) * 1e-3
+    if scheme == "gfd":   # the lone forward launch, timed in the separate-call runs above
+        t_trace = separate["forward_ms"] * 1e-3
+        tr_ms = [separate["forward_ms"]]
     alg_bytes = crossings_local * BYTES_PER_CROSSING + n * BYTES_PER_GEODESIC
     achieved = alg_bytes / t_trace / 1e9
     traffic = profile_traffic(key, n)
@@ -513,7 +551,7 @@ def measure(key, args, ctx, headline):
         gather = {"gather": mesh.gather, "record_bytes": 3 * mesh.nf * 128, "achieved_grecords_per_s": cps_fwd / 1e9,
                   "peak_grecords_per_s": peak_g, "frac": cps_fwd / 1e9 / peak_g,
                   "source": "scripts/micro/gather_bench run inside this bench before the timed region"}
-    bwd_ms = float(np.mean(step_ms) - np.mean(tr_ms))
+    bwd_ms = float(np.mean(step_ms) - np.mean(tr_ms)) if scheme != "gfd" else separate["ms_per_step"] - separate["forward_ms"]
     line = {"metric": f"face_crossings_per_s_fwd_{scheme}" if scheme != "fwd" else "face_crossings_per_s_fwd",
             "value": value, "unit": "face-crossings/s", "n_gpus": world, "steps": steps, "warmup": warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
@@ -541,6 +579,24 @@ def measure(key, args, ctx, headline):
                                               "d2h_bytes_per_step": int(lean_out),
                                               "note": "same call, NULL for the outputs a training step does not read"}},
             "gpu_launches": launches, "clocks": clocks.summary()}
+    if scheme == "gfd":
+        # the kernel that IS the fused step: round 2 with the forward traces as fourth sibling of every sample's three
+        # re-traces (4n full-length jobs); timed as the whole dg_trace_gfd call (job builders, eps-length seeds / par
+        # jobs and the assembly ride along: < 3 % of it), so the fraction is a lower bound for the kernel's own
+        t_fused = float(np.mean(step_ms)) * 1e-3
+        alg4 = 4 * crossings_local * BYTES_PER_CROSSING + 4 * n * BYTES_PER_GEODESIC
+        info4 = dg.kernel_info(False, False, cached=mesh.has_transport_cache, dense=True)
+        tr4 = profile_traffic(key + "_gfd_fused", n)
+        line["fused_forward_gfd"] = {"ms": float(np.mean(step_ms)), "note": "dg_trace_gfd + dg_gfd_pullback: the step `value` is quoted on",
+                                     "roofline": {"bound": "hbm", "achieved": alg4 / t_fused / 1e9, "peak": peak, "unit": "GB/s",
+                                                  "frac": alg4 / t_fused / 1e9 / peak,
+                                                  "traffic": tr4["dram_bytes_per_launch"] if tr4 else None,
+                                                  "kernel": "trace_fast_kernel<crossing records, 256-bit loads, sibling groups of 4>",
+                                                  "algorithmic_bytes_per_launch": alg4, "registers": info4["registers"],
+                                                  "blocks_per_sm": info4["blocks_per_sm"]}}
+        line["separate_calls"] = {"ms_per_step": separate["ms_per_step"], "forward_ms": separate["forward_ms"],
+                                  "value": crossings_local / (separate["ms_per_step"] * 1e-3),
+                                  "note": "rank 0, lone forward launch + GFD with the forward results as known base"}
     if scheme == "gfd":
         # the kernel that takes most of a GFD step: round 2, three full-length re-traces per sample as sibling groups
         # (+ n eps-length jobs). Its duration is rank 0's backward time (job builders, seeds and assembly are < 2 % of

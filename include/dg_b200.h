@@ -305,6 +305,25 @@ DG_API int dg_gfd_jacobians_with_base(const dg_mesh* mesh, int64_t n, const int3
                                       uint8_t* degraded, double* frames, double* grad_v,
                                       double* grad_p, int64_t* err_index);
 
+/* Forward exp map AND GFD Jacobians of the same samples in ONE call. GFD's base trace of a sample is its forward
+ * trace (diff.cpp:288-294: (p, v), no payload), and the Jacobians do not depend on the upstream gradient, so a
+ * training step that will differentiate with GFD runs its forward here: the base traces ride in GFD's round 2 as the
+ * FOURTH SIBLING of their sample's three full-length re-traces (the lanes of a group follow the same faces step for
+ * step and share every crossing-record fetch), which costs less than half of a lone forward launch. *fwd receives the
+ * forward results exactly as dg_trace_batch writes them (face, bary, dir, traced, requested, term, status, stall,
+ * npoints, crossings, total_crossings; same bits; payload / transport / poly_* must be NULL), jv / jp / degraded /
+ * frames as dg_gfd_jacobians. The backward of the step is then dg_gfd_pullback. When GFD fails as a whole
+ * (DG_ERR_DEGENERATE_DIRECTION, DG_ERR_GFD ...) the forward results are still valid. */
+DG_API int dg_trace_gfd(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
+                        double eps_v, double eps_p, const dg_diff_cfg* cfg, dg_trace_out* fwd, double* jv, double* jp,
+                        uint8_t* degraded, double* frames, int64_t* err_index);
+/* pullback_ambient (diff.cpp:342-354) of upstream gradients g[3n] through GFD Jacobians that are already there
+ * (jv, jp of dg_trace_gfd / dg_gfd_jacobians; end_face = the forward end faces): grad_v, grad_p [3n]. One light
+ * kernel; DG_MEM_DEVICE: asynchronous on cfg->stream. Same bits as passing g to dg_gfd_jacobians. */
+DG_API int dg_gfd_pullback(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* v, const int32_t* end_face,
+                           const double* jv, const double* jp, const double* g, const dg_diff_cfg* cfg, double* grad_v,
+                           double* grad_p);
+
 /* ---- resident batch (forward + backward on the same samples) --------------------------------
  * A training step runs trace_batch (tracer.hpp:94) and then the EP loop ep_jacobians +
  * pullback_ambient (gradcheck.cpp:76-89) or gfd_batched_many (gradcheck.cpp:74) on the SAME
@@ -321,6 +340,11 @@ DG_API int64_t dg_batch_size(const dg_batch* b);
  * through dg_trace_batch). cfg->memory must be DG_MEM_HOST and cfg->stream NULL. */
 DG_API int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg,
                           dg_trace_out* out);
+/* The forward of a step whose backward will be GFD: dg_trace_gfd on the resident batch (forward results out, the
+ * Jacobians stay on the GPU). A following dg_batch_gfd with the same eps and step limit only pulls g back. A
+ * whole-call GFD failure is reported by that dg_batch_gfd call, not here: the forward results are valid. */
+DG_API int dg_batch_trace_gfd(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, double eps_v,
+                              double eps_p, dg_trace_out* out);
 /* EP backward of the resident samples: g [3n] in, grad_v [3n] (and grad_p [3n], zero) out. */
 DG_API int dg_batch_ep_backward(dg_batch* b, const double* g, double* grad_v, double* grad_p,
                                 int64_t* err_index);

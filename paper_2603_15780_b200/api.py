@@ -346,6 +346,69 @@ class Mesh:
                                      ptr(grad_v), ptr(grad_p), None, None, None, C.addressof(ei)), ei)
 
 
+    # ------------------------------------------ fused forward + GFD Jacobians, pull-back only backward
+    def trace_gfd(self, face, bary, dirs, eps_v=None, eps_p=None, max_steps=0, plain_schedule=False):
+        """dg_trace_gfd on host arrays: the forward exp map and the GFD Jacobians of the same samples in one call
+        (the forward traces ride in GFD's round 2 as the fourth sibling). Returns (TraceResult, dict jv/jp/degraded/
+        frames). A whole-call GFD failure raises AFTER the forward results are in place (`.forward` of the error)."""
+        h = self._handle()
+        face, bary, dirs = _i32(face), _f64(bary), _f64(dirs)
+        n = len(face)
+        eps = self.default_gfd_eps()
+        eps_v = eps if eps_v is None else eps_v
+        eps_p = eps if eps_p is None else eps_p
+        r = TraceResult(face=np.empty(n, np.int32), bary=np.empty((n, 3)), dir=np.empty((n, 3)), traced=np.empty(n),
+                        requested=np.empty(n), term=np.empty(n, np.uint8), status=np.empty(n, np.uint8),
+                        stall=np.empty(n, np.uint8), npoints=np.empty(n, np.int32), crossings=np.empty(n, np.int32))
+        jac = dict(jv=np.zeros((n, 4)), jp=np.zeros((n, 4)), degraded=np.zeros((n, 4), np.uint8),
+                   frames=np.zeros((n, capi.FRAME_DOUBLES)))
+        total = C.c_uint64(0)
+        o = TraceOut(ptr(r.face), ptr(r.bary), ptr(r.dir), ptr(r.traced), ptr(r.requested), ptr(r.term), ptr(r.status),
+                     ptr(r.stall), None, None, ptr(r.npoints), ptr(r.crossings), C.addressof(total), None, 0, None, None, None)
+        cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps), schedule=int(plain_schedule))
+        ei = C.c_int64(-1)
+        rc = lib().dg_trace_gfd(h, n, ptr(face), ptr(bary), ptr(dirs), float(eps_v), float(eps_p), C.addressof(cfg),
+                                C.addressof(o), ptr(jac["jv"]), ptr(jac["jp"]), ptr(jac["degraded"]), ptr(jac["frames"]),
+                                C.addressof(ei))
+        r.total_crossings = int(total.value)
+        r.errors = [(int(i), capi.STALL_MESSAGES[int(r.stall[i])]) for i in np.nonzero(r.status)[0]]
+        if rc != capi.DG_OK:
+            e = DgError(rc, lib().dg_last_error().decode())
+            e.index = ei.value
+            e.forward = r
+            raise e
+        return r, jac
+
+    def trace_gfd_device(self, face, bary, dirs, out, eps_v, eps_p, jv, jp, degraded=None, stream=None, max_steps=0):
+        """dg_trace_gfd on torch CUDA tensors; `out` as trace_batch_device."""
+        import torch
+        cfg = DiffCfg(memory=capi.MEM_DEVICE, max_steps=int(max_steps),
+                      stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
+        o = TraceOut()
+        for k, v in out.items():
+            setattr(o, k, ptr(v))
+        ei = C.c_int64(-1)
+        check(lib().dg_trace_gfd(self._handle(), int(face.numel()), ptr(face), ptr(bary), ptr(dirs), float(eps_v), float(eps_p),
+                                 C.addressof(cfg), C.addressof(o), ptr(jv), ptr(jp), ptr(degraded), None, C.addressof(ei)), ei)
+
+    def gfd_pullback(self, face, v, end_face, jv, jp, g):
+        """pullback_ambient of g through Jacobians that are already there (dg_gfd_pullback), host arrays."""
+        face, end_face, v, jv, jp, g = _i32(face), _i32(end_face), _f64(v), _f64(jv), _f64(jp), _f64(g)
+        n = len(face)
+        out = dict(grad_v=np.zeros((n, 3)), grad_p=np.zeros((n, 3)))
+        cfg = DiffCfg(memory=capi.MEM_HOST)
+        check(lib().dg_gfd_pullback(self._handle(), n, ptr(face), ptr(v), ptr(end_face), ptr(jv), ptr(jp), ptr(g),
+                                    C.addressof(cfg), ptr(out["grad_v"]), ptr(out["grad_p"])))
+        return out
+
+    def gfd_pullback_device(self, face, v, end_face, jv, jp, g, grad_v, grad_p=None, stream=None):
+        import torch
+        cfg = DiffCfg(memory=capi.MEM_DEVICE,
+                      stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
+        check(lib().dg_gfd_pullback(self._handle(), int(face.numel()), ptr(face), ptr(v), ptr(end_face), ptr(jv), ptr(jp), ptr(g),
+                                    C.addressof(cfg), ptr(grad_v), ptr(grad_p)))
+
+
 # dg_trace_cfg.walker (DG_WALKER_*): which kernel traces a plain f64 forward request
 WALKERS = {"auto": 0, "generic": 1, "loads": 2, "tma": 3, "coop": 4}
 
@@ -372,7 +435,11 @@ class Batch:
         except Exception:  # interpreter shutdown: the library handle may already be gone
             pass
 
-    def trace(self, face, bary, dirs, max_steps=0, refill_min=0, blocks_per_sm=0, out=None):
+    def trace(self, face, bary, dirs, max_steps=0, refill_min=0, blocks_per_sm=0, out=None, gfd=False, eps_v=None,
+              eps_p=None):
+        """gfd=True: the forward of a step whose backward will be GFD (dg_batch_trace_gfd): the Jacobians are
+        computed with the forward traces (fourth sibling of GFD's round 2) and stay on the GPU; the following
+        Batch.gfd(g=...) with the same eps only pulls g back."""
         face, bary, dirs = _i32(face), _f64(bary), _f64(dirs)
         n = len(face)
         if bary.size != 3 * n or dirs.size != 3 * n:
@@ -389,7 +456,12 @@ class Batch:
         o = TraceOut(ptr(r.face), ptr(r.bary), ptr(r.dir), ptr(r.traced), ptr(r.requested), ptr(r.term),
                      ptr(r.status), ptr(r.stall), None, None, ptr(r.npoints), ptr(r.crossings),
                      C.addressof(total), None, 0, None, None, None)
-        check(lib().dg_batch_trace(self._h, n, C.addressof(tin), C.addressof(cfg), C.addressof(o)))
+        if gfd:
+            eps = self.mesh.default_gfd_eps()
+            check(lib().dg_batch_trace_gfd(self._h, n, C.addressof(tin), C.addressof(cfg), float(eps if eps_v is None else eps_v),
+                                           float(eps if eps_p is None else eps_p), C.addressof(o)))
+        else:
+            check(lib().dg_batch_trace(self._h, n, C.addressof(tin), C.addressof(cfg), C.addressof(o)))
         r.total_crossings = int(total.value)
         return r
 

@@ -38,8 +38,8 @@ EXPORTS = [
     "dg_mesh_device_count", "dg_device_sm_count",
     "dg_mesh_derive", "dg_mesh_create", "dg_mesh_create_ex", "dg_mesh_has_transport_cache", "dg_mesh_uses_tma_gather", "dg_mesh_gather_mode", "dg_mesh_destroy", "dg_mesh_face_count", "dg_mesh_vertex_count",
     "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_trace_polylines", "dg_transition", "dg_ep_jacobians",
-    "dg_ep_backward", "dg_gfd_jacobians", "dg_gfd_jacobians_with_base", "dg_trace_kernel_info",
-    "dg_batch_create", "dg_batch_destroy", "dg_batch_size", "dg_batch_trace", "dg_batch_ep_backward", "dg_batch_gfd",
+    "dg_ep_backward", "dg_gfd_jacobians", "dg_gfd_jacobians_with_base", "dg_trace_gfd", "dg_gfd_pullback", "dg_trace_kernel_info",
+    "dg_batch_create", "dg_batch_destroy", "dg_batch_size", "dg_batch_trace", "dg_batch_trace_gfd", "dg_batch_ep_backward", "dg_batch_gfd",
 ]
 
 
@@ -117,6 +117,9 @@ def lib():
         L.dg_ep_backward.argtypes = [vp, i64] + [vp] * 9
         L.dg_gfd_jacobians.argtypes = [vp, i64, vp, vp, vp, dbl, dbl] + [vp] * 12
         L.dg_gfd_jacobians_with_base.argtypes = [vp, i64] + [vp] * 8 + [dbl, dbl] + [vp] * 9
+        L.dg_trace_gfd.argtypes = [vp, i64, vp, vp, vp, dbl, dbl] + [vp] * 7
+        L.dg_gfd_pullback.argtypes = [vp, i64] + [vp] * 9
+        L.dg_batch_trace_gfd.argtypes = [vp, i64, vp, vp, dbl, dbl, vp]
         L.dg_trace_kernel_info.argtypes = [C.c_int, C.c_int, vp, vp, vp]
         L.dg_trace_kernel_info.restype = None
         L.dg_batch_create.argtypes = [vp, i64, vp]

@@ -34,6 +34,14 @@ struct dg_batch {
   std::vector<dgapi::Shard> shards;
   std::vector<dg_batch*> subs;
   int64_t n_total = 0;
+  // dg_batch_trace_gfd: the GFD Jacobians of the resident samples are on the device already (jv, jp, degraded);
+  // a whole-call GFD failure of that forward is kept for the backward call to report
+  bool gfd_ready = false;
+  double gfd_eps_v = 0, gfd_eps_p = 0;
+  int32_t gfd_steps = 0;
+  int gfd_rc = 0;
+  int64_t gfd_err_index = -1;
+  std::string gfd_msg;
 };
 
 namespace {
@@ -143,6 +151,7 @@ int dgapi::batch_trace_one(dg_batch* b, int64_t n, const dg_trace_in* in, const 
   DeviceGuard guard(b->mesh->device);
   if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
   b->traced = false;
+  b->gfd_ready = false;
   b->shards.clear();
   b->n = n;
   b->traced_max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(b->mesh->nf);
@@ -204,6 +213,76 @@ int dgapi::batch_trace_one(dg_batch* b, int64_t n, const dg_trace_in* in, const 
   return DG_OK;
 }
 
+// Forward of a GFD step (dg_trace_gfd on the resident arrays): inputs in, forward + Jacobians in one pass, forward
+// results out; the Jacobians stay. One stream: the sibling launch is the step, there is nothing to pipeline against.
+static int batch_trace_gfd_one(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, double eps_v,
+                               double eps_p, dg_trace_out* out) {
+  if (!b) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace_gfd: missing batch");
+  if (n < 0 || n > b->cap) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace_gfd: batch size exceeds the capacity");
+  if (!in || !out) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace_gfd: null request or result block");
+  if (n > 0 && (!in->face || !in->bary || !in->dir))
+    return fail(DG_ERR_INVALID_ARGS, "trace_batch: starts and dirs differ in length");
+  dg_trace_cfg c{};
+  if (cfg) c = *cfg;
+  if (in->payload || out->payload || out->transport || out->poly_offsets || c.want_transport_matrix || c.hole_avoidance || c.use_f32)
+    return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace_gfd: the plain f64 forward map only");
+  if (c.memory != DG_MEM_HOST || c.stream) return fail(DG_ERR_INVALID_ARGS, "dg_batch_trace_gfd: host pointers, library streams");
+  DeviceGuard guard(b->mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
+  b->traced = false;
+  b->gfd_ready = false;
+  b->shards.clear();
+  b->n = n;
+  b->traced_max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(b->mesh->nf);
+  b->traced_f32 = false;
+  if (n == 0) {
+    if (out->total_crossings) *out->total_crossings = 0;
+    b->traced = true;
+    return DG_OK;
+  }
+  const size_t N = size_t(n), C = size_t(b->cap);
+  cudaError_t e = cudaSuccess;
+  auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  if (!b->jv) { note(dev_alloc(&b->jv, 4 * C)); note(dev_alloc(&b->jp, 4 * C)); note(dev_alloc(&b->degraded, 4 * C)); }
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_trace_gfd");
+  cudaStream_t st = b->streams[0];
+  note(cudaMemcpyAsync(b->face, in->face, N * 4, cudaMemcpyHostToDevice, st));
+  note(cudaMemcpyAsync(b->bary, in->bary, N * 24, cudaMemcpyHostToDevice, st));
+  note(cudaMemcpyAsync(b->dir, in->dir, N * 24, cudaMemcpyHostToDevice, st));
+  dg_diff_cfg dc{};
+  dc.memory = DG_MEM_DEVICE;
+  dc.stream = st;
+  dc.max_steps = c.max_steps;
+  dg_trace_out dout{};
+  dout.face = b->o_face; dout.bary = b->o_bary; dout.dir = b->o_dir; dout.traced = b->o_traced; dout.requested = b->o_requested;
+  dout.term = b->o_term; dout.status = b->o_status; dout.stall = b->o_stall;
+  dout.npoints = out->npoints ? b->o_npoints : nullptr;
+  dout.crossings = out->crossings ? b->o_crossings : nullptr;
+  dout.total_crossings = out->total_crossings ? b->totals : nullptr;
+  int64_t idx = -1;
+  const int rc = gfd_jacobians_impl(b->mesh, n, b->face, b->bary, b->dir, eps_v, eps_p, nullptr, &dc, b->jv, b->jp, b->degraded,
+                                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &idx, nullptr, &dout);
+  if (rc == DG_ERR_CUDA || rc == DG_ERR_INVALID_ARGS || rc == DG_ERR_NO_DEVICE) return rc;
+  b->gfd_rc = rc;   // a whole-call GFD failure: the forward results are valid, the backward call reports it
+  b->gfd_err_index = idx;
+  b->gfd_msg = rc != DG_OK ? last_error() : std::string();
+  auto back = [&](auto* host, const auto* dev, size_t stride) {
+    if (host) note(cudaMemcpyAsync(host, dev, N * stride * sizeof(*host), cudaMemcpyDeviceToHost, st));
+  };
+  back(out->face, b->o_face, 1); back(out->bary, b->o_bary, 3); back(out->dir, b->o_dir, 3);
+  back(out->traced, b->o_traced, 1); back(out->requested, b->o_requested, 1);
+  back(out->term, b->o_term, 1); back(out->status, b->o_status, 1); back(out->stall, b->o_stall, 1);
+  back(out->npoints, b->o_npoints, 1); back(out->crossings, b->o_crossings, 1);
+  if (out->total_crossings) note(cudaMemcpyAsync(&b->words[0], b->totals, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  note(cudaStreamSynchronize(st));
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_trace_gfd");
+  if (out->total_crossings) *out->total_crossings = b->words[0];
+  b->traced = true;
+  b->gfd_ready = true;
+  b->gfd_eps_v = eps_v; b->gfd_eps_p = eps_p; b->gfd_steps = b->traced_max_steps;
+  return DG_OK;
+}
+
 // EP backward (diff.cpp:44-66, 328-354) on the resident samples: g in, grad_v (and grad_p) out.
 static int batch_ep_backward_one(dg_batch* b, const double* g, double* grad_v, double* grad_p, int64_t* err_index) {
   if (err_index) *err_index = -1;
@@ -255,9 +334,35 @@ static int batch_gfd_one(dg_batch* b, double eps_v, double eps_p, const double* 
   const size_t N = size_t(n), C = size_t(b->cap);
   cudaError_t e = cudaSuccess;
   auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  cudaStream_t st = b->streams[0];
+  const int32_t want_steps = max_steps > 0 ? max_steps : default_max_steps(b->mesh->nf);
+  if (b->gfd_ready && b->gfd_eps_v == eps_v && b->gfd_eps_p == eps_p && b->gfd_steps == want_steps) {
+    // the forward of this step was dg_batch_trace_gfd: the Jacobians are resident, the backward is the pull-back
+    if (b->gfd_rc != DG_OK) {
+      if (err_index) *err_index = b->gfd_err_index;
+      last_error() = b->gfd_msg;
+      return b->gfd_rc;
+    }
+    if (g) {
+      note(cudaMemcpyAsync(b->g, g, N * 24, cudaMemcpyHostToDevice, st));
+      dg::GfdPullback pb{};
+      pb.mesh = b->mesh->view();
+      pb.n = n;
+      pb.face = b->face; pb.v = b->dir; pb.end_face = b->o_face; pb.jv = b->jv; pb.jp = b->jp; pb.g = b->g;
+      pb.grad_v = grad_v ? b->grad_v : nullptr; pb.grad_p = grad_p ? b->grad_p : nullptr;
+      note(dg::launch_gfd_pullback(pb, st));
+      if (grad_v) note(cudaMemcpyAsync(grad_v, b->grad_v, N * 24, cudaMemcpyDeviceToHost, st));
+      if (grad_p) note(cudaMemcpyAsync(grad_p, b->grad_p, N * 24, cudaMemcpyDeviceToHost, st));
+    }
+    if (jv) note(cudaMemcpyAsync(jv, b->jv, N * 32, cudaMemcpyDeviceToHost, st));
+    if (jp) note(cudaMemcpyAsync(jp, b->jp, N * 32, cudaMemcpyDeviceToHost, st));
+    if (degraded) note(cudaMemcpyAsync(degraded, b->degraded, N * 4, cudaMemcpyDeviceToHost, st));
+    note(cudaStreamSynchronize(st));
+    if (e != cudaSuccess) return fail_cuda(e, "dg_batch_gfd");
+    return DG_OK;
+  }
   if (!b->jv) { note(dev_alloc(&b->jv, 4 * C)); note(dev_alloc(&b->jp, 4 * C)); note(dev_alloc(&b->degraded, 4 * C)); }
   if (e != cudaSuccess) return fail_cuda(e, "dg_batch_gfd");
-  cudaStream_t st = b->streams[0];
   if (g) note(cudaMemcpyAsync(b->g, g, N * 24, cudaMemcpyHostToDevice, st));
   dg_diff_cfg dc{};
   dc.memory = DG_MEM_DEVICE;
@@ -290,9 +395,14 @@ static dg_batch* shard_batch(dg_batch* b, int k) { return k == 0 ? b : b->subs[s
 
 extern "C" {
 
-int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, dg_trace_out* out) {
+}  // extern "C"
+
+// the forward of a resident batch over the devices of a multi-GPU mesh; run_one runs a shard on its device's batch
+template <class One>
+static int batch_trace_dispatch(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, dg_trace_out* out,
+                                One run_one) {
   if (!b || !in || !out || n > b->cap || !fan_out(b->mesh, n) || !in->dir || (cfg && cfg->memory != DG_MEM_HOST))
-    return batch_trace_one(b, n, in, cfg, out);
+    return run_one(b, n, in, cfg, out);
   const std::vector<Shard> shards = cut_shards(b->mesh, n, in->dir);
   const int S = int(shards.size());
   b->subs.resize(size_t(S) - 1, nullptr);
@@ -316,7 +426,7 @@ int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace
     so.term = at(out->term, one); so.status = at(out->status, one); so.stall = at(out->stall, one);
     so.npoints = at(out->npoints, one); so.crossings = at(out->crossings, one);
     so.total_crossings = out->total_crossings ? &totals[size_t(k)] : nullptr;
-    return batch_trace_one(shard_batch(b, k), s.n, &sin, cfg, &so);
+    return run_one(shard_batch(b, k), s.n, &sin, cfg, &so);
   });
   if (rc != DG_OK) { b->traced = false; return rc; }
   if (out->total_crossings) {
@@ -328,6 +438,19 @@ int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace
   b->n_total = n;
   b->traced = true;
   return DG_OK;
+}
+
+extern "C" {
+
+int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, dg_trace_out* out) {
+  return batch_trace_dispatch(b, n, in, cfg, out, [](dg_batch* sb, int64_t m, const dg_trace_in* i, const dg_trace_cfg* c,
+                                                     dg_trace_out* o) { return batch_trace_one(sb, m, i, c, o); });
+}
+
+int dg_batch_trace_gfd(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg, double eps_v, double eps_p,
+                       dg_trace_out* out) {
+  return batch_trace_dispatch(b, n, in, cfg, out, [=](dg_batch* sb, int64_t m, const dg_trace_in* i, const dg_trace_cfg* c,
+                                                      dg_trace_out* o) { return batch_trace_gfd_one(sb, m, i, c, eps_v, eps_p, o); });
 }
 
 int dg_batch_ep_backward(dg_batch* b, const double* g, double* grad_v, double* grad_p, int64_t* err_index) {

@@ -171,7 +171,8 @@ struct GfdKnownBase {
 int gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
                        double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
                        uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
-                       double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* known_base);
+                       double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* known_base,
+                       const dg_trace_out* fwd = nullptr);
 
 // EP backward on device-resident arrays without a host round trip: *err_word (device) receives
 // kEpNoError or (sample index << 2 | reason), decoded by ep_error_to_rc after the stream is synced.

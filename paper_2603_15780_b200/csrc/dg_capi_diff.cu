@@ -15,10 +15,18 @@ int check_common(const dg_mesh* mesh, int64_t n, const char* who) {
 }
 
 // Runs one batch of trace jobs that already live on the device (GFD rounds).
+// The forward result record the base traces of a fused forward + GFD call write (they are the jobs [from, n) of
+// round 2): what dg_trace_batch reports beyond end face / barycentrics / direction / termination / status.
+struct AuxOut {
+  int64_t from = 0;
+  double* traced = nullptr; double* requested = nullptr; uint8_t* stall = nullptr;
+  int32_t* npoints = nullptr; int32_t* crossings = nullptr;
+};
+
 cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const double* jb, const double* jd,
                      const double* jp, int32_t* rf, double* rb, double* rd, double* rp, uint8_t* rt, uint8_t* rs,
                      int max_steps, unsigned long long* total, cudaStream_t stream, int siblings = 0,
-                     int64_t sibling_stride = 0) {
+                     int64_t sibling_stride = 0, const AuxOut* aux = nullptr) {
   if (n <= 0) return cudaSuccess;
   dg::TraceParams p{};
   mesh->bind(p);
@@ -28,6 +36,11 @@ cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const do
   p.max_steps = max_steps;
   p.refill_min = 0;  // the walker's own default
   p.siblings = siblings; p.sibling_stride = sibling_stride;
+  if (aux) {
+    p.aux_from = aux->from;
+    p.o_traced = aux->traced; p.o_requested = aux->requested; p.o_stall = aux->stall;
+    p.o_npoints = aux->npoints; p.o_crossings = aux->crossings;
+  }
   unsigned long long* ctr = mesh->next_counters();
   p.queue_head = ctr;
   p.total_crossings = total;
@@ -187,10 +200,11 @@ int dg_ep_backward(const dg_mesh* mesh, int64_t n, const int32_t* face, const do
 static int gfd_dispatch(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
                         double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
                         uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
-                        double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* kb) {
+                        double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* kb,
+                        const dg_trace_out* fwd = nullptr) {
   if (!mesh || !fan_out(mesh, n) || !face || !bary || !v)
     return dgapi::gfd_jacobians_impl(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
-                                     base_face, base_bary, base_dir, err_index, kb);
+                                     base_face, base_bary, base_dir, err_index, kb, fwd);
   if (err_index) *err_index = -1;
   dg_diff_cfg c{};
   if (cfg) c = *cfg;
@@ -205,18 +219,33 @@ static int gfd_dispatch(const dg_mesh* mesh, int64_t n, const int32_t* face, con
   std::vector<int64_t> idx(shards.size(), -1);
   std::vector<int> rcs(shards.size(), DG_OK);
   std::vector<std::string> msgs(shards.size());
+  std::vector<uint64_t> totals(shards.size(), 0);   // host mode: per-shard forward totals (fused forward)
+  unsigned long long* dev_totals = nullptr;         // device mode: the same on the primary device
+  if (fwd && fwd->total_crossings && dev) {
+    DeviceGuard guard(mesh->device);
+    DG_CUDA(cudaMalloc(reinterpret_cast<void**>(&dev_totals), shards.size() * sizeof(unsigned long long)));
+    DG_CUDA(cudaMemsetAsync(dev_totals, 0, shards.size() * sizeof(unsigned long long), static_cast<cudaStream_t>(c.stream)));
+  }
   run_shards(shards, [&](const Shard& s, int k) {
     const size_t L = size_t(s.lo), M = size_t(s.n);
     auto at = [&](auto* p, size_t stride) { return p ? p + stride * L : p; };
     dg_diff_cfg sc = c;
     int r;
+    dg_trace_out sf{};
+    if (fwd) {
+      sf.face = at(fwd->face, 1); sf.bary = at(fwd->bary, 3); sf.dir = at(fwd->dir, 3); sf.traced = at(fwd->traced, 1);
+      sf.requested = at(fwd->requested, 1); sf.term = at(fwd->term, 1); sf.status = at(fwd->status, 1);
+      sf.stall = at(fwd->stall, 1); sf.npoints = at(fwd->npoints, 1); sf.crossings = at(fwd->crossings, 1);
+      if (fwd->total_crossings) sf.total_crossings = dev ? reinterpret_cast<uint64_t*>(dev_totals + k) : &totals[size_t(k)];
+    }
     if (s.mesh == mesh || !dev) {
       if (s.mesh != mesh) sc.stream = nullptr;
       GfdKnownBase skb{};
       if (kb) skb = GfdKnownBase{at(kb->face, 1), at(kb->bary, 3), at(kb->dir, 3), at(kb->term, 1), at(kb->status, 1)};
       r = dgapi::gfd_jacobians_impl(s.mesh, s.n, at(face, 1), at(bary, 3), at(v, 3), eps_v, eps_p, at(g, 3), &sc, at(jv, 4),
                                     at(jp, 4), at(degraded, 4), at(frames, DG_FRAME_DOUBLES), at(grad_v, 3), at(grad_p, 3),
-                                    at(base_face, 1), at(base_bary, 3), at(base_dir, 3), &idx[size_t(k)], kb ? &skb : nullptr);
+                                    at(base_face, 1), at(base_bary, 3), at(base_dir, 3), &idx[size_t(k)], kb ? &skb : nullptr,
+                                    fwd ? &sf : nullptr);
     } else {
       DeviceGuard work(s.mesh->device);
       cudaStream_t ws = s.mesh->stream;
@@ -226,12 +255,19 @@ static int gfd_dispatch(const dg_mesh* mesh, int64_t n, const int32_t* face, con
       GfdKnownBase skb{};
       if (kb) skb = GfdKnownBase{ps.in(at(kb->face, 1), M), ps.in(at(kb->bary, 3), 3 * M), ps.in(at(kb->dir, 3), 3 * M),
                                  ps.in(at(kb->term, 1), M), ps.in(at(kb->status, 1), M)};
+      dg_trace_out lf{};
+      if (fwd) {
+        lf.face = ps.out(sf.face, M); lf.bary = ps.out(sf.bary, 3 * M); lf.dir = ps.out(sf.dir, 3 * M);
+        lf.traced = ps.out(sf.traced, M); lf.requested = ps.out(sf.requested, M); lf.term = ps.out(sf.term, M);
+        lf.status = ps.out(sf.status, M); lf.stall = ps.out(sf.stall, M); lf.npoints = ps.out(sf.npoints, M);
+        lf.crossings = ps.out(sf.crossings, M); lf.total_crossings = ps.out(sf.total_crossings, 1);
+      }
       r = dgapi::gfd_jacobians_impl(s.mesh, s.n, ps.in(at(face, 1), M), ps.in(at(bary, 3), 3 * M), ps.in(at(v, 3), 3 * M), eps_v,
                                     eps_p, ps.in(at(g, 3), 3 * M), &sc, ps.out(at(jv, 4), 4 * M), ps.out(at(jp, 4), 4 * M),
                                     ps.out(at(degraded, 4), 4 * M), ps.out(at(frames, DG_FRAME_DOUBLES), size_t(DG_FRAME_DOUBLES) * M),
                                     ps.out(at(grad_v, 3), 3 * M), ps.out(at(grad_p, 3), 3 * M), ps.out(at(base_face, 1), M),
                                     ps.out(at(base_bary, 3), 3 * M), ps.out(at(base_dir, 3), 3 * M), &idx[size_t(k)],
-                                    kb ? &skb : nullptr);
+                                    kb ? &skb : nullptr, fwd ? &lf : nullptr);
       ps.flush();
       ps.note(cudaStreamSynchronize(ws));
       if (r == DG_OK && ps.error() != cudaSuccess) r = fail_cuda(ps.error(), "dg_gfd_jacobians peer copies");
@@ -241,6 +277,19 @@ static int gfd_dispatch(const dg_mesh* mesh, int64_t n, const int32_t* face, con
     return DG_OK;
   });
   if (ready) cudaEventDestroy(ready);
+  if (fwd && fwd->total_crossings) {   // (every shard has synchronised its stream: these entry points are host-synchronous)
+    uint64_t t = 0;
+    if (dev) {
+      DeviceGuard guard(mesh->device);
+      cudaMemcpy(totals.data(), dev_totals, totals.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+      for (uint64_t x : totals) t += x;
+      cudaMemcpy(fwd->total_crossings, &t, sizeof t, cudaMemcpyHostToDevice);
+      cudaFree(dev_totals);
+    } else {
+      for (uint64_t x : totals) t += x;
+      *fwd->total_crossings = t;
+    }
+  }
   // whole-call failures in the reference's order (diff.cpp:273-326): every sample's frames are built before any
   // trace runs, so a degenerate direction anywhere wins over a failed base trace; then request order
   int pick = -1;
@@ -259,6 +308,43 @@ int dg_gfd_jacobians(const dg_mesh* mesh, int64_t n, const int32_t* face, const 
                      double* base_bary, double* base_dir, int64_t* err_index) {
   return gfd_dispatch(mesh, n, face, bary, v, eps_v, eps_p, g, cfg, jv, jp, degraded, frames, grad_v, grad_p,
                       base_face, base_bary, base_dir, err_index, nullptr);
+}
+
+int dg_trace_gfd(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v, double eps_v,
+                 double eps_p, const dg_diff_cfg* cfg, dg_trace_out* fwd, double* jv, double* jp, uint8_t* degraded,
+                 double* frames, int64_t* err_index) {
+  if (!fwd) return fail(DG_ERR_INVALID_ARGS, "dg_trace_gfd: null forward result block");
+  if (fwd->payload || fwd->transport || fwd->poly_offsets)
+    return fail(DG_ERR_INVALID_ARGS, "dg_trace_gfd: the plain forward map only (payload / transport matrix / polylines: dg_trace_batch)");
+  return gfd_dispatch(mesh, n, face, bary, v, eps_v, eps_p, nullptr, cfg, jv, jp, degraded, frames, nullptr, nullptr, nullptr,
+                      nullptr, nullptr, err_index, nullptr, fwd);
+}
+
+int dg_gfd_pullback(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* v, const int32_t* end_face,
+                    const double* jv, const double* jp, const double* g, const dg_diff_cfg* cfg, double* grad_v,
+                    double* grad_p) {
+  if (int e = check_common(mesh, n, "dg_gfd_pullback")) return e;
+  if (n == 0) return DG_OK;
+  if (!face || !v || !end_face || !jv || !jp || !g) return fail(DG_ERR_INVALID_ARGS, "dg_gfd_pullback: null argument");
+  dg_diff_cfg c{};
+  if (cfg) c = *cfg;
+  const bool device_mode = c.memory == DG_MEM_DEVICE;
+  DeviceGuard guard(mesh->device);
+  if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
+  cudaStream_t stream = (device_mode || c.stream) ? static_cast<cudaStream_t>(c.stream) : mesh->stream;
+  Stage st(stream, device_mode);
+  const size_t N = size_t(n);
+  dg::GfdPullback b{};
+  b.mesh = mesh->view();
+  b.n = n;
+  b.face = st.in(face, N); b.v = st.in(v, 3 * N); b.end_face = st.in(end_face, N);
+  b.jv = st.in(jv, 4 * N); b.jp = st.in(jp, 4 * N); b.g = st.in(g, 3 * N);
+  b.grad_v = st.out(grad_v, 3 * N); b.grad_p = st.out(grad_p, 3 * N);
+  if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_gfd_pullback staging");
+  st.note(dg::launch_gfd_pullback(b, stream));
+  cudaError_t e = st.finish();   // device mode: asynchronous on the caller's stream
+  if (e != cudaSuccess) return fail_cuda(e, "dg_gfd_pullback");
+  return DG_OK;
 }
 
 int dg_gfd_jacobians_with_base(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
@@ -303,9 +389,11 @@ int dgapi::ep_error_to_rc(unsigned long long word, const char* who, int64_t* err
 int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, const double* v,
                               double eps_v, double eps_p, const double* g, const dg_diff_cfg* cfg, double* jv, double* jp,
                               uint8_t* degraded, double* frames, double* grad_v, double* grad_p, int32_t* base_face,
-                              double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* known_base) {
+                              double* base_bary, double* base_dir, int64_t* err_index, const GfdKnownBase* known_base,
+                              const dg_trace_out* fwd) {
   if (err_index) *err_index = -1;
   if (int e = check_common(mesh, n, "dg_gfd_jacobians")) return e;
+  if (fwd && known_base) return fail(DG_ERR_INVALID_ARGS, "dg_trace_gfd: the forward traces are this call's own base traces");
   if (n == 0) return DG_OK;
   if (!face || !bary || !v) return fail(DG_ERR_INVALID_ARGS, "dg_gfd_jacobians: null argument");
   dg_diff_cfg c{};
@@ -362,7 +450,17 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
     b.par_face = par_rface; b.par_bary = par_rbary; b.par_term = par_rterm; b.par_status = par_rstatus;
   }
   b.err = st.scratch<unsigned long long>(8);
+  // fused forward (dg_trace_gfd): the base jobs [3n, 4n) of round 2 write the rest of the forward result record
+  AuxOut aux;
+  unsigned long long* fwd_total = nullptr;
+  if (fwd) {
+    aux.from = 3 * n;
+    aux.traced = st.out(fwd->traced, N); aux.requested = st.out(fwd->requested, N); aux.stall = st.out(fwd->stall, N);
+    aux.npoints = st.out(fwd->npoints, N); aux.crossings = st.out(fwd->crossings, N);
+    if (fwd->total_crossings) fwd_total = st.scratch<unsigned long long>(1);
+  }
   if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_gfd_jacobians staging");
+  if (fwd_total) st.note(cudaMemsetAsync(fwd_total, 0, sizeof(unsigned long long), stream));
 
   unsigned long long h_err[8];
   for (auto& w : h_err) w = kNoError;
@@ -381,7 +479,7 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
                      b.r2_term, b.r2_status, max_steps, nullptr, stream, group ? 3 : 0, n));
   } else {
     st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, r2_dir, nullptr,
-                     b.r2_term, b.r2_status, max_steps, nullptr, stream, group ? 4 : 0, n));
+                     b.r2_term, b.r2_status, max_steps, fwd_total, stream, group ? 4 : 0, n, fwd ? &aux : nullptr));
     st.note(dg::launch_gfd_par_jobs(b, stream));
     st.note(run_jobs(mesh, n, b.par_jface, b.par_jbary, b.par_jdir, nullptr, par_rface, par_rbary, nullptr, nullptr,
                      par_rterm, par_rstatus, max_steps, nullptr, stream));
@@ -418,6 +516,14 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   if (base_face) st.note(cudaMemcpyAsync(base_face, b.base_face, N * sizeof(int32_t), kind, stream));
   if (base_bary) st.note(cudaMemcpyAsync(base_bary, b.base_bary, 3 * N * sizeof(double), kind, stream));
   if (base_dir) st.note(cudaMemcpyAsync(base_dir, b.base_dir, 3 * N * sizeof(double), kind, stream));
+  if (fwd) {   // the forward results of the samples = the end states of the base traces
+    if (fwd->face) st.note(cudaMemcpyAsync(fwd->face, b.base_face, N * sizeof(int32_t), kind, stream));
+    if (fwd->bary) st.note(cudaMemcpyAsync(fwd->bary, b.base_bary, 3 * N * sizeof(double), kind, stream));
+    if (fwd->dir) st.note(cudaMemcpyAsync(fwd->dir, b.base_dir, 3 * N * sizeof(double), kind, stream));
+    if (fwd->term) st.note(cudaMemcpyAsync(fwd->term, b.base_term, N, kind, stream));
+    if (fwd->status) st.note(cudaMemcpyAsync(fwd->status, b.base_status, N, kind, stream));
+    if (fwd_total) st.note(cudaMemcpyAsync(fwd->total_crossings, fwd_total, sizeof(uint64_t), kind, stream));
+  }
   cudaError_t e = st.finish();
   if (e != cudaSuccess) return fail_cuda(e, "dg_gfd_jacobians");
 

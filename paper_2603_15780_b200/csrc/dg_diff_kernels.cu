@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(128) gfd_round1_jobs_kernel(const __grid_const
     note_error(b.err + 0, i);
     for (int k = 0; k < 2; ++k) put_job(b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, k * n + i, f, p, zero, zero);
     put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, 2 * n + i, f, p, zero, zero);
-    if (b.base_in_round2) put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, 3 * n + i, f, p, zero, zero);
+    // (the base job keeps the sample's own v: with a fused forward its record is the forward result of the sample)
+    if (b.base_in_round2) put_job(b.j2_face, b.j2_bary, b.j2_dir, nullptr, 3 * n + i, f, p, v, zero);
     return;
   }
   const BaryFrame fp = make_bary_frame(load_face<double>(b.mesh, f));
@@ -313,6 +314,27 @@ __global__ void __launch_bounds__(128) gfd_assemble_kernel(const __grid_constant
     if (b.grad_v) st3(b.grad_v, i, fv.e_par * gv0 + fv.e_perp * gv1);
     if (b.grad_p) st3(b.grad_p, i, fp.pinv0 * gp0 + fp.pinv1 * gp1);
   }
+}
+
+// pullback_ambient through GFD Jacobians that are already there (diff.cpp:342-354): the last block of
+// gfd_assemble_kernel on its own, same expressions, same bits. One thread per sample.
+__global__ void __launch_bounds__(128) gfd_pullback_kernel(const __grid_constant__ GfdPullback b) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= b.n) return;
+  const int f = b.face[i], fe = b.end_face[i];
+  if (f < 0 || f >= b.mesh.nf || fe < 0 || fe >= b.mesh.nf) return;
+  TangentFrame fv;
+  if (!make_tangent_frame(b.mesh, f, ld3(b.v, i), &fv)) return;
+  const BaryFrame fp = make_bary_frame(load_face<double>(b.mesh, f));
+  const BaryFrame fo = make_bary_frame(load_face<double>(b.mesh, fe));
+  const double* jv = b.jv + 4 * i;
+  const double* jp = b.jp + 4 * i;
+  const V g = ld3(b.g, i);
+  const double go0 = dot(fo.u_hat, g), go1 = dot(fo.v_hat, g);
+  const double gv0 = jv[0] * go0 + jv[2] * go1, gv1 = jv[1] * go0 + jv[3] * go1;
+  const double gp0 = jp[0] * go0 + jp[2] * go1, gp1 = jp[1] * go0 + jp[3] * go1;
+  if (b.grad_v) st3(b.grad_v, i, fv.e_par * gv0 + fv.e_perp * gv1);
+  if (b.grad_p) st3(b.grad_p, i, fp.pinv0 * gp0 + fp.pinv1 * gp1);
 }
 
 __global__ void __launch_bounds__(128) gfd_fallback_jobs_kernel(const __grid_constant__ GfdBuffers b) {
@@ -485,6 +507,11 @@ cudaError_t launch_gfd_par_jobs(const GfdBuffers& b, cudaStream_t stream) {
 }
 cudaError_t launch_gfd_assemble(const GfdBuffers& b, cudaStream_t stream) {
   gfd_assemble_kernel<0><<<grid_for(b.n, 128), 128, 0, stream>>>(b);
+  return cudaGetLastError();
+}
+cudaError_t launch_gfd_pullback(const GfdPullback& b, cudaStream_t stream) {
+  if (b.n <= 0) return cudaSuccess;
+  gfd_pullback_kernel<<<unsigned((b.n + 127) / 128), 128, 0, stream>>>(b);
   return cudaGetLastError();
 }
 cudaError_t launch_gfd_fallback_jobs(const GfdBuffers& b, cudaStream_t stream) {

@@ -34,6 +34,10 @@ struct TraceParams {
   double* o_transport;
   int32_t* o_npoints;
   int32_t* o_crossings;
+  // o_traced / o_requested / o_stall / o_npoints / o_crossings and total_crossings cover the queries q >= aux_from
+  // only, at index q - aux_from (0: every query). GFD's fused forward: the base traces are the last quarter of
+  // round 2's jobs, and only they write the forward result record.
+  int64_t aux_from;
   const int64_t* poly_offsets;  // non-null: record polylines, trace q from slot poly_offsets[q]
   int32_t poly_cap;             // > 0 (poly_offsets null): record polylines, trace q owns slots [q cap, (q + 1) cap);
                                 // points beyond are counted in o_npoints but not written (dg_trace_polylines, pass 1)
@@ -130,6 +134,15 @@ struct GfdBuffers {
   // [4] first stalled fallback trace
   unsigned long long* err;
 };
+// pull-back of upstream gradients through resident GFD Jacobians (dg_gfd_pullback)
+struct GfdPullback {
+  MeshView mesh;
+  int64_t n;
+  const int32_t* face; const double* v; const int32_t* end_face;
+  const double* jv; const double* jp; const double* g;
+  double* grad_v; double* grad_p;
+};
+cudaError_t launch_gfd_pullback(const GfdPullback& b, cudaStream_t stream);
 cudaError_t launch_gfd_round1_jobs(const GfdBuffers& b, cudaStream_t stream);
 cudaError_t launch_gfd_round2_jobs(const GfdBuffers& b, cudaStream_t stream);
 cudaError_t launch_gfd_par_jobs(const GfdBuffers& b, cudaStream_t stream);

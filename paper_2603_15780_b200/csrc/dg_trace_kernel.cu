@@ -46,13 +46,13 @@ __device__ __forceinline__ void write_result(const TraceParams& p, int64_t q,
     V3<double> d = T.target > S(0) ? cast<double>(T.dir) : V3<double>{0.0, 0.0, 0.0};
     p.o_dir[3 * q] = d.x; p.o_dir[3 * q + 1] = d.y; p.o_dir[3 * q + 2] = d.z;
   }
-  if (p.o_traced) p.o_traced[q] = T.traced;
-  if (p.o_requested) p.o_requested[q] = double(T.target);
+  if (p.o_traced && q >= p.aux_from) p.o_traced[q - p.aux_from] = T.traced;
+  if (p.o_requested && q >= p.aux_from) p.o_requested[q - p.aux_from] = double(T.target);
   if (p.o_term) p.o_term[q] = T.term;
   if (p.o_status) p.o_status[q] = T.status;
-  if (p.o_stall) p.o_stall[q] = T.stall_code;
-  if (p.o_npoints) p.o_npoints[q] = T.npoints;
-  if (p.o_crossings) p.o_crossings[q] = T.crossings;
+  if (p.o_stall && q >= p.aux_from) p.o_stall[q - p.aux_from] = T.stall_code;
+  if (p.o_npoints && q >= p.aux_from) p.o_npoints[q - p.aux_from] = T.npoints;
+  if (p.o_crossings && q >= p.aux_from) p.o_crossings[q - p.aux_from] = T.crossings;
   if (kFull) {
     if (p.o_payload) {
       V3<double> w = T.has_payload ? cast<double>(T.payload) : V3<double>{0.0, 0.0, 0.0};
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kBlockThreads, kFull ? DG_TRACE_MIN_BLOCKS_FUL
     if (live) {
       live = T.run_step();
       if (!live) {
-        my_crossings += (unsigned long long)T.crossings;
+        if (q >= p.aux_from) my_crossings += (unsigned long long)T.crossings;
         write_result<S, kFull, kCached>(p, q, T);
       }
     }

@@ -258,3 +258,68 @@ def test_single_transitions(gpu, ref):
         rf, rb, rv = pm.transition(2, fb[i], bb[i], dv[i])
         assert o["rc"][i] == 0 and rf == o["face"][i]
         assert np.array_equal(rb, o["bary"][i]) and np.array_equal(rv, o["v"][i])
+
+
+def test_fused_forward_gfd_and_pullback_give_the_bits_of_the_separate_calls(gpu, ref):
+    """dg_trace_gfd: the forward traces ride in GFD's round 2 as the fourth sibling of their sample's re-traces and
+    write the forward result record; dg_gfd_pullback pulls an upstream gradient back through the resident Jacobians.
+    Forward results == dg_trace_batch, Jacobians == dg_gfd_jacobians, gradients == dg_gfd_jacobians with g -- all
+    bit for bit, on both mesh layouts, incl. a batch with rejected / stalled / zero-length starts in the forward
+    record and an open mesh where the one-sided fallback rounds run; and through the resident batch."""
+    rng = np.random.default_rng(8)
+    for rm, n, cache in ((ref.RefMesh.torus(1 / 3, 1 / 6, 64, 32), 5003, True), (ref.RefMesh.icosphere(3), 2000, False)):
+        a = rm.arrays()
+        m = gpu.Mesh(a["xyz"], a["tri"], transport_cache=cache)
+        f, b, d = rm.sample_queries(31, n, 0.05, 0.9)
+        g = unit_rows(rng, n)
+        fwd = m.trace_batch(f, b, d)
+        sep = m.gfd(f, b, d, g=g)
+        r, jac = m.trace_gfd(f, b, d)
+        for k in ("face", "bary", "dir", "traced", "requested", "term", "status", "stall", "npoints", "crossings"):
+            assert np.array_equal(getattr(r, k), getattr(fwd, k)), k
+        assert r.total_crossings == fwd.total_crossings
+        for k in ("jv", "jp", "degraded", "frames"):
+            assert np.array_equal(jac[k], sep[k]), k
+        pb = m.gfd_pullback(f, d, r.face, jac["jv"], jac["jp"], g)
+        assert np.array_equal(pb["grad_v"], sep["grad_v"]) and np.array_equal(pb["grad_p"], sep["grad_p"])
+        # resident batch: forward with gfd=True, then the backward is the pull-back
+        bt = gpu.Batch(m, n)
+        rb = bt.trace(f, b, d, gfd=True)
+        for k in ("face", "bary", "dir", "traced", "requested", "term", "status", "stall", "npoints", "crossings"):
+            assert np.array_equal(getattr(rb, k), getattr(fwd, k)), k
+        out = bt.gfd(g=g)
+        for k in ("jv", "jp", "degraded", "grad_v", "grad_p"):
+            assert np.array_equal(out[k], sep[k]), k
+        out2 = bt.gfd(g=2 * g)   # another upstream gradient, same Jacobians
+        assert np.array_equal(out2["grad_v"], m.gfd(f, b, d, g=2 * g)["grad_v"])
+        bt.close()
+    # the forward record of starts GFD cannot differentiate: the whole-call error comes with valid forward results
+    rm = ref.RefMesh.icosphere(2)
+    m = gpu_mesh(gpu, rm)
+    f, b, d = rm.sample_queries(3, 64, 0.3, 1.0)
+    d[5] = 0.0                                   # zero-length request: DegenerateDirection for GFD
+    d[9] = rm.arrays()["fnormal"][f[9]]          # normal to the anchor face: stalls in the forward
+    fwd = m.trace_batch(f, b, d)
+    with pytest.raises(gpu.DgError) as e:
+        m.trace_gfd(f, b, d)
+    assert e.value.klass == "DegenerateDirection" and e.value.index == 5
+    for k in ("face", "bary", "dir", "traced", "requested", "term", "status", "stall"):
+        assert np.array_equal(getattr(e.value.forward, k), getattr(fwd, k)), k
+    # open mesh: base traces that leave the mesh -> "gfd: the base trace did not reach its requested length"
+    pm = ref.RefMesh.plane(6, 6, 1.0, 0)
+    mp = gpu_mesh(gpu, pm)
+    f, b, d = pm.sample_queries(4, 500, 0.5, 2.0)
+    fwd = mp.trace_batch(f, b, d)
+    assert (fwd.term == 1).any()
+    with pytest.raises(gpu.DgError) as e:
+        mp.trace_gfd(f, b, d)
+    assert e.value.klass == "Error" and "base trace" in e.value.msg
+    assert np.array_equal(e.value.forward.bary, fwd.bary) and np.array_equal(e.value.forward.term, fwd.term)
+    keep = (fwd.term == 0) & (fwd.status == 0)
+    P = pm.embed(f, b)
+    keep &= (P[:, :2].min(1) > 0.02) & (P[:, :2].max(1) < 0.98)
+    f, b, d = f[keep], b[keep], d[keep]
+    sep = mp.gfd(f, b, d)
+    r, jac = mp.trace_gfd(f, b, d)
+    for k in ("jv", "jp", "degraded"):
+        assert np.array_equal(jac[k], sep[k]), k
