@@ -10,7 +10,7 @@ config 2 (bumpy sphere, icosphere-6 displaced radially, 81 920 faces; 1 M geodes
 0.5 x bbox diagonal; forward + EP). The same JSON line carries one block per further configuration of
 BASELINE.json under "blocks" -- c3 (1 M-face noisy torus, 10 M geodesics in all, forward + GFD, the SAME batch
 sharded over the N GPUs: strong scaling), c4 (64 concatenated meshes, 65 536 queries each, mixed lengths) and
-c5 (1 M-face torus, length 5 x diameter, half vertex / edge starts, 12.5 M geodesics per GPU) -- each with its
+c5 (1 M-face torus, length 5 x diameter, half vertex-to-vertex walks, 2.5 M geodesics per GPU) -- each with its
 own value, roofline, e2e and cpu_baseline. With --gpus N > 1 and no torchrun environment the script starts
 its N ranks itself (torch.distributed.run, one process per GPU). Prints ONE JSON line.
 """
@@ -39,8 +39,11 @@ WORKLOADS = {
                scheme="gfd", n=10_000_000, scaling="strong", max_steps=0),
     "c4": dict(name="64 meshes of 10k-200k faces concatenated (6.8M faces), 65,536 queries per mesh, lengths log-uniform in "
                     "[0.01, 2] x bbox diagonal, forward", scheme="fwd", n=64 * 65536, scaling="strong", max_steps=0),
-    "c5": dict(name="torus 1000x500 (1,000,000 faces), geodesics of length 5 x outer diameter, half exactly at vertices "
-                    "along an edge, max_steps 200000, forward", scheme="fwd", n=12_500_000, scaling="weak", max_steps=200_000),
+    # (config 5 is 100 M queries on 8 GPUs = 12.5 M per GPU; a bench step runs a fifth of one GPU's share -- 2.5 M
+    # geodesics, 1.5e10 face crossings, two seconds of walker -- so that the default run stays within minutes)
+    "c5": dict(name="torus 1000x500 (1,000,000 faces), 2.5M geodesics per GPU of length 5 x outer diameter, half exactly at "
+                    "vertices along a meridian edge (vertex-to-vertex walks), max_steps 200000, forward",
+               scheme="fwd", n=2_500_000, scaling="weak", max_steps=200_000),
 }
 
 

@@ -74,6 +74,7 @@ enum { DG_EVENT_ADVANCED = 0, DG_EVENT_CROSSED_EDGE = 1, DG_EVENT_CROSSED_VERTEX
        DG_EVENT_BOUNDARY_SLIDE = 3, DG_EVENT_BOUNDARY_STOP = 4 };
 
 enum { DG_MEM_HOST = 0, DG_MEM_DEVICE = 1 };
+enum { DG_SORT_AUTO = 0, DG_SORT_ON = 1, DG_SORT_OFF = 2 };
 enum { DG_WALKER_AUTO = 0, DG_WALKER_GENERIC = 1, DG_WALKER_FAST_LOADS = 2, DG_WALKER_FAST_TMA = 3, DG_WALKER_FAST_COOP = 4 };
 /* Arithmetic of the f64 tracer: there is ONE lane. The library is built without FMA contraction
  * and follows the reference's operation order, so a trace that never takes a vertex branch (no
@@ -157,7 +158,9 @@ typedef struct dg_trace_cfg {
   uint8_t lane;                  /* reserved (see DG_LANE_*) */
   uint8_t memory;                /* DG_MEM_HOST: pointers are host memory, staged by the library
                                     DG_MEM_DEVICE: pointers are device memory on the mesh's GPU */
-  uint8_t sort_by_face;          /* schedule queries in start-face order (results stay at request index) */
+  uint8_t sort_by_face;          /* DG_SORT_*: schedule queries in start-face order (results stay at the request index,
+                                    same bits). AUTO = on for batches >= 32 768 on meshes whose crossing records exceed
+                                    the L2 (> 96 MB), where neighbouring starts share their fetches; off otherwise */
   uint8_t refill_min;            /* idle lanes a warp waits for before it steals work (0 = the walker's default:
                                     4 with a bounded wait for the fast walker, 1 for the general one) */
   uint8_t blocks_per_sm;         /* resident CTAs per SM of the persistent grid (0 = occupancy query) */

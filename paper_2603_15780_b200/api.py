@@ -145,7 +145,7 @@ class Mesh:
 
     # ------------------------------------------------------------------ forward tracing
     def trace_batch(self, face, bary, dirs, payload=None, max_steps=0, hole_avoidance=False, want_q=False,
-                    record_polyline=False, use_f32=False, sort_by_face=False, refill_min=0, blocks_per_sm=0,
+                    record_polyline=False, use_f32=False, sort_by_face=None, refill_min=0, blocks_per_sm=0,
                     out=None, generic_walker=False, walker="auto", two_call_polylines=False, poly_views=False):
         """trace_batch (tracer.cpp:596) on host arrays; results at the request index. `out`: a
         TraceResult of a previous call of the same size whose (e.g. pinned) arrays are reused.
@@ -171,7 +171,7 @@ class Mesh:
             r.q = np.empty((n, 9))
         cfg = TraceCfg(max_steps=int(max_steps), hole_avoidance=int(hole_avoidance),
                        want_transport_matrix=int(want_q), use_f32=int(use_f32), memory=capi.MEM_HOST,
-                       sort_by_face=int(sort_by_face), refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm),
+                       sort_by_face=SORT[sort_by_face], refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm),
                        walker=1 if generic_walker else WALKERS[walker])
         tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), ptr(payload))
         total = C.c_uint64(0)
@@ -182,7 +182,7 @@ class Mesh:
                            C.addressof(total), ptr(off), tot, ptr(pf), ptr(pb), ptr(ps))
             check(lib().dg_trace_batch(h, n, C.addressof(tin), C.addressof(cfg), C.addressof(out)))
 
-        if record_polyline and not two_call_polylines and not sort_by_face:
+        if record_polyline and not two_call_polylines and sort_by_face is not True:
             out_s = TraceOut(ptr(r.face), ptr(r.bary), ptr(r.dir), ptr(r.traced), ptr(r.requested), ptr(r.term),
                              ptr(r.status), ptr(r.stall), ptr(r.payload), ptr(r.q), ptr(r.npoints), ptr(r.crossings),
                              C.addressof(total), None, 0, None, None, None)
@@ -216,7 +216,7 @@ class Mesh:
         return r
 
     def trace_batch_device(self, face, bary, dirs, out, payload=None, max_steps=0, hole_avoidance=False,
-                           want_q=False, stream=None, sort_by_face=False, refill_min=0, blocks_per_sm=0,
+                           want_q=False, stream=None, sort_by_face=None, refill_min=0, blocks_per_sm=0,
                            generic_walker=False, walker="auto"):
         """Zero-copy entry point: every array is a torch CUDA tensor on the mesh's device;
         `out` maps dg_trace_out field names to preallocated tensors. Asynchronous on `stream`."""
@@ -224,7 +224,7 @@ class Mesh:
         h = self._handle()
         n = int(face.numel())
         cfg = TraceCfg(max_steps=int(max_steps), hole_avoidance=int(hole_avoidance),
-                       want_transport_matrix=int(want_q), memory=capi.MEM_DEVICE, sort_by_face=int(sort_by_face),
+                       want_transport_matrix=int(want_q), memory=capi.MEM_DEVICE, sort_by_face=SORT[sort_by_face],
                        refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm),
                        walker=1 if generic_walker else WALKERS[walker],
                        stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
@@ -409,6 +409,8 @@ class Mesh:
                                     C.addressof(cfg), ptr(grad_v), ptr(grad_p)))
 
 
+# dg_trace_cfg.sort_by_face (DG_SORT_*): None = the library decides
+SORT = {None: 0, "auto": 0, True: 1, False: 2, 1: 1, 0: 2}
 # dg_trace_cfg.walker (DG_WALKER_*): which kernel traces a plain f64 forward request
 WALKERS = {"auto": 0, "generic": 1, "loads": 2, "tma": 3, "coop": 4}
 
