@@ -135,6 +135,11 @@ DG_API int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, 
                              const int32_t* adj, const double* fnormal, const double* vangle,
                              const uint8_t* vboundary, const int32_t* csr_off,
                              const int32_t* csr_list, uint32_t flags, dg_mesh** out);
+/* Memory the library keeps warm: its own stream-ordered pool per device for staging buffers (never the device's
+ * default pool, which other frameworks of the process use), a resident batch behind large DG_MEM_HOST calls, the
+ * small-batch blocks and the pinned polyline arrays of a mesh. dg_trim releases all of it (m may be NULL: only the
+ * pool of the current device); everything is re-created on demand. */
+DG_API int dg_trim(const dg_mesh* m);
 DG_API int dg_mesh_has_transport_cache(const dg_mesh* m);
 /* How the fast walker gathers this mesh's crossing records for a batch of lone traces
  * (DG_WALKER_AUTO): per-lane 256-bit loads (also: no records), TMA tile::gather4, or cooperative
@@ -252,6 +257,11 @@ DG_API int dg_transition(const dg_mesh* mesh, int which, int64_t n, const int32_
 /* frames block per sample: e_par, e_perp, normal (frame_in_v) | u_hat, v_hat, pinv_row0,
  * pinv_row1 (frame_in_p) | the same four for frame_out */
 
+/* DG_MEM_DEVICE with the differentials: the pointers are device memory and the work runs on cfg->stream, but
+ * dg_ep_jacobians, dg_ep_backward, dg_gfd_jacobians[_with_base] and dg_trace_gfd are HOST-SYNCHRONOUS: their
+ * return code depends on an error word of the batch (first degenerate sample, failed base trace ...), so they wait
+ * for cfg->stream before they return, and must not be called under stream capture. dg_gfd_pullback and
+ * dg_trace_batch are asynchronous on the stream. */
 typedef struct dg_diff_cfg {
   uint8_t memory;       /* DG_MEM_HOST / DG_MEM_DEVICE for all pointers of the call */
   uint8_t lane;         /* reserved (see DG_LANE_*) */

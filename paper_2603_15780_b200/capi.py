@@ -35,7 +35,7 @@ STALL_MESSAGES = {
 
 EXPORTS = [
     "dg_last_error", "dg_version", "dg_device_count", "dg_set_device", "dg_set_devices", "dg_set_device_list",
-    "dg_mesh_device_count", "dg_device_sm_count",
+    "dg_mesh_device_count", "dg_device_sm_count", "dg_trim",
     "dg_mesh_derive", "dg_mesh_create", "dg_mesh_create_ex", "dg_mesh_has_transport_cache", "dg_mesh_uses_tma_gather", "dg_mesh_gather_mode", "dg_mesh_destroy", "dg_mesh_face_count", "dg_mesh_vertex_count",
     "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_trace_polylines", "dg_transition", "dg_ep_jacobians",
     "dg_ep_backward", "dg_gfd_jacobians", "dg_gfd_jacobians_with_base", "dg_trace_gfd", "dg_gfd_pullback", "dg_trace_kernel_info",
@@ -104,6 +104,7 @@ def lib():
         L.dg_set_devices.argtypes = [C.c_uint64]
         L.dg_set_device_list.argtypes = [vp, i32]
         L.dg_mesh_device_count.argtypes = [vp]
+        L.dg_trim.argtypes = [vp]
         L.dg_mesh_derive.argtypes = [vp, i32, vp, i32] + [vp] * 11
         L.dg_mesh_create.argtypes = [vp, i32, vp, i32] + [vp] * 7
         L.dg_mesh_create_ex.argtypes = [vp, i32, vp, i32] + [vp] * 6 + [C.c_uint32, vp]

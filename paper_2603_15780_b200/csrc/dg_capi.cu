@@ -105,9 +105,21 @@ bool encode_record_map(const dg::HalfEdgeRec* he, size_t rows, unsigned char* ou
   return true;
 }
 
-__global__ void iota_kernel(int32_t* a, int64_t n) {
+// Scheduling key of query i and its own index: start face, plus one bit above the face bits for starts that
+// snap_bary will put ON A VERTEX (tracer.cpp:148-161). Such traces begin in the vertex branch -- and, aimed along an
+// edge, stay in it vertex after vertex (config 5) --, which runs through the general state machine; a warp that
+// mixes them with plain edge-crossing traces executes both paths one after the other (c5, 1 M geodesics: 853 ms
+// mixed, 506 ms with the two kinds in warps of their own). A schedule only: results stay at the request index.
+__global__ void sort_keys_kernel(const int32_t* __restrict__ face, const double* __restrict__ bary, int64_t n, int32_t nf,
+                                 int bits, int32_t* keys, int32_t* index) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) a[i] = int32_t(i);
+  if (i >= n) return;
+  const int32_t f = face[i];
+  const double b0 = bary[3 * i], b1 = bary[3 * i + 1], b2 = bary[3 * i + 2];
+  const double hi = 1.0 - 1e-10;
+  const bool vertex = b0 >= hi || b1 >= hi || b2 >= hi;
+  keys[i] = (f >= 0 && f < nf ? f : 0) | (vertex ? (int32_t(1) << bits) : 0);
+  index[i] = int32_t(i);
 }
 
 }  // namespace
@@ -324,15 +336,6 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
 #define DG_TRY(expr) if ((e = (expr)) != cudaSuccess) return cleanup(fail_cuda(e, #expr))
   DG_TRY(cudaDeviceGetAttribute(&m->sm_count, cudaDevAttrMultiProcessorCount, g_device));
   DG_TRY(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
-  {
-    // Staging buffers come from the device's stream-ordered pool; keep freed blocks cached so
-    // that a DG_MEM_HOST call does not pay for physical allocation on every invocation.
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, g_device) == cudaSuccess) {
-      unsigned long long keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-  }
   const size_t F = size_t(nf), Vn = size_t(nv);
   DG_TRY(cudaMalloc(&m->rec, F * sizeof(dg::FaceRec)));
   DG_TRY(cudaMalloc(&m->fnormal, 3 * F * sizeof(double)));
@@ -340,7 +343,6 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   DG_TRY(cudaMalloc(&m->csr_off, (Vn + 1) * sizeof(int32_t)));
   DG_TRY(cudaMalloc(&m->csr_list, 3 * F * sizeof(int32_t)));
   DG_TRY(cudaMalloc(&m->vboundary, Vn));
-  DG_TRY(cudaMalloc(&m->counters, 2 * dg_mesh::kRing * sizeof(unsigned long long)));
   m->bytes = int64_t(F * sizeof(dg::FaceRec) + 3 * F * 8 + Vn * 8 + (Vn + 1) * 4 + 3 * F * 4 + Vn);
   // Transport cache policy (384 B per face on top of the 96 B face record).
   bool cache = (flags & 3u) == DG_MESH_TRANSPORT_ON;
@@ -366,9 +368,9 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   // indexed arrays are only needed to assemble the records
   double* d_xyz = nullptr;
   int32_t *d_tri = nullptr, *d_adj = nullptr;
-  DG_TRY(cudaMallocAsync(&d_xyz, 3 * Vn * sizeof(double), m->stream));
-  DG_TRY(cudaMallocAsync(&d_tri, 3 * F * sizeof(int32_t), m->stream));
-  DG_TRY(cudaMallocAsync(&d_adj, 3 * F * sizeof(int32_t), m->stream));
+  DG_TRY(pool_alloc(reinterpret_cast<void**>(&d_xyz), 3 * Vn * sizeof(double), m->stream));
+  DG_TRY(pool_alloc(reinterpret_cast<void**>(&d_tri), 3 * F * sizeof(int32_t), m->stream));
+  DG_TRY(pool_alloc(reinterpret_cast<void**>(&d_adj), 3 * F * sizeof(int32_t), m->stream));
   DG_TRY(cudaMemcpyAsync(d_xyz, xyz, 3 * Vn * sizeof(double), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(d_tri, tri, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(d_adj, adj, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
@@ -383,7 +385,6 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   DG_TRY(cudaMemcpyAsync(m->csr_off, csr_off, (Vn + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(m->csr_list, csr_list, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(m->vboundary, vboundary, Vn, cudaMemcpyHostToDevice, m->stream));
-  DG_TRY(cudaMemsetAsync(m->counters, 0, 2 * dg_mesh::kRing * sizeof(unsigned long long), m->stream));
   DG_TRY(cudaFreeAsync(d_xyz, m->stream));
   DG_TRY(cudaFreeAsync(d_tri, m->stream));
   DG_TRY(cudaFreeAsync(d_adj, m->stream));
@@ -430,9 +431,44 @@ void dg_mesh_destroy(dg_mesh* m) {
   if (m->small_pin) cudaFreeHost(m->small_pin);
   cudaFree(m->small_dev);
   cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
-  cudaFree(m->csr_list); cudaFree(m->vboundary); cudaFree(m->counters);
+  cudaFree(m->csr_list); cudaFree(m->vboundary);
   if (m->stream) cudaStreamDestroy(m->stream);
   delete m;
+}
+
+// Releases what the library keeps warm between calls: the mesh's hidden buffers (the resident batch behind large
+// DG_MEM_HOST calls, the small-batch blocks, the pinned polyline arrays; m may be NULL) and the cached blocks of the
+// library's staging pool on the mesh's device (or the current device). They are re-created on demand.
+int dg_trim(const dg_mesh* m) {
+  int device = g_device;
+  if (m) {
+    device = m->device;
+    DeviceGuard guard(m->device);
+    cudaStreamSynchronize(m->stream);
+    {
+      std::lock_guard<std::mutex> lock(m->host_batch_mu);
+      if (m->host_batch) dg_batch_destroy(m->host_batch);
+      m->host_batch = nullptr;
+      m->host_batch_cap = 0;
+    }
+    {
+      std::lock_guard<std::mutex> lock(m->small_mu);
+      if (m->small_pin) cudaFreeHost(m->small_pin);
+      cudaFree(m->small_dev);
+      m->small_pin = m->small_dev = nullptr;
+      m->small_cap = 0;
+      m->small_cursors_clean = false;
+    }
+    {
+      std::lock_guard<std::mutex> lock(m->poly_mu);
+      poly_store_free(m->poly);
+      m->poly = nullptr;
+    }
+    for (const dg_mesh* copy : m->replicas) dg_trim(copy);
+  }
+  if (dg_device_count() == 0) return DG_OK;
+  if (cudaMemPool_t pool = staging_pool(device)) cudaMemPoolTrimTo(pool, 0);
+  return DG_OK;
 }
 
 int dg_mesh_has_transport_cache(const dg_mesh* m) { return m && m->he ? 1 : 0; }
@@ -604,7 +640,9 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   p.hole_avoidance = c.hole_avoidance;
   p.want_q = c.want_transport_matrix;
 
-  unsigned long long* ctr = mesh->next_counters();
+  // the work cursor and the crossing total of THIS call, stream-ordered like the rest of its staging
+  unsigned long long* ctr = st.scratch<unsigned long long>(2);
+  if (!ctr) return fail_cuda(st.error(), "dg_trace_batch staging");
   p.queue_head = ctr;
   p.total_crossings = total_dst ? ctr + 1 : nullptr;
   st.note(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), stream));
@@ -618,17 +656,18 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   const bool big_mesh = mesh->he && size_t(3) * size_t(mesh->nf) * sizeof(dg::HalfEdgeRec) > (size_t(96) << 20);
   const bool sort = c.sort_by_face == DG_SORT_ON || (c.sort_by_face == DG_SORT_AUTO && big_mesh && n >= (int64_t(1) << 15) && !record);
   if (sort) {
+    int32_t* keys_in = st.scratch<int32_t>(N);
     int32_t* keys_out = st.scratch<int32_t>(N);
     int32_t* iota = st.scratch<int32_t>(N);
     int32_t* perm = st.scratch<int32_t>(N);
-    if (keys_out && iota && perm) {
-      iota_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(iota, n);
-      size_t tmp_bytes = 0;
+    if (keys_in && keys_out && iota && perm) {
       int bits = 1;
-      while ((int64_t(1) << bits) < int64_t(mesh->nf) && bits < 31) ++bits;
-      st.note(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, p.face, keys_out, iota, perm, int(n), 0, bits, stream));
+      while ((int64_t(1) << bits) < int64_t(mesh->nf) && bits < 30) ++bits;
+      sort_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(p.face, p.bary, n, mesh->nf, bits, keys_in, iota);
+      size_t tmp_bytes = 0;
+      st.note(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, iota, perm, int(n), 0, bits + 1, stream));
       void* tmp = st.scratch<char>(tmp_bytes);
-      if (tmp) st.note(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, p.face, keys_out, iota, perm, int(n), 0, bits, stream));
+      if (tmp) st.note(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, iota, perm, int(n), 0, bits + 1, stream));
       p.perm = perm;
     }
   }
@@ -760,7 +799,7 @@ static int trace_batch_multi_device(const dg_mesh* mesh, int64_t n, const dg_tra
   DG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   unsigned long long* parts = nullptr;
   if (out->total_crossings) {
-    DG_CUDA(cudaMallocAsync(&parts, size_t(S) * sizeof(unsigned long long), home));
+    DG_CUDA(pool_alloc(reinterpret_cast<void**>(&parts), size_t(S) * sizeof(unsigned long long), home));
     DG_CUDA(cudaMemsetAsync(parts, 0, size_t(S) * sizeof(unsigned long long), home));
   }
   DG_CUDA(cudaEventRecord(ready, home));

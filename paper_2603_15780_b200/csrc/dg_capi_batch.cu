@@ -49,6 +49,15 @@ namespace {
 template <class T>
 cudaError_t dev_alloc(T** p, size_t count) { return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)); }
 
+cudaError_t ensure_backward(dg_batch* b) {
+  if (b->g) return cudaSuccess;
+  const size_t N = size_t(b->cap);
+  cudaError_t e = dev_alloc(&b->g, 3 * N);
+  if (e == cudaSuccess) e = dev_alloc(&b->grad_v, 3 * N);
+  if (e == cudaSuccess) e = dev_alloc(&b->grad_p, 3 * N);
+  return e;
+}
+
 int slices_for(int64_t n) {
   if (const char* env = getenv("DG_BATCH_SLICES")) return std::max(1, std::min(dg_batch::kStreams, atoi(env)));
   if (n >= (int64_t(1) << 18)) return 4;
@@ -104,7 +113,8 @@ int dgapi::batch_create_one(const dg_mesh* mesh, int64_t capacity, dg_batch** ou
   ok(dev_alloc(&b->o_npoints, N)); ok(dev_alloc(&b->o_crossings, N));
   ok(dev_alloc(&b->totals, size_t(dg_batch::kStreams)));
   ok(cudaMallocHost(reinterpret_cast<void**>(&b->words), dg_batch::kStreams * sizeof(uint64_t)));
-  ok(dev_alloc(&b->g, 3 * N)); ok(dev_alloc(&b->grad_v, 3 * N)); ok(dev_alloc(&b->grad_p, 3 * N));
+  // (the backward buffers g / grad_v / grad_p are allocated by the first backward call: a forward-only user --
+  // the resident batch behind large DG_MEM_HOST dg_trace_batch calls -- never pays for them)
   if (e != cudaSuccess) {
     dg_batch_destroy(b);
     return fail_cuda(e, "dg_batch_create");
@@ -293,7 +303,8 @@ static int batch_ep_backward_one(dg_batch* b, const double* g, double* grad_v, d
   DeviceGuard guard(b->mesh->device);
   if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
   const int S = slices_for(n);
-  cudaError_t e = cudaSuccess;
+  cudaError_t e = ensure_backward(b);
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_ep_backward");
   auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   // per slice: g in, fused kernel, gradients out -- nothing waits on the host until every slice is queued
   // (totals[] doubles as the per-slice error words)
@@ -332,7 +343,8 @@ static int batch_gfd_one(dg_batch* b, double eps_v, double eps_p, const double* 
   DeviceGuard guard(b->mesh->device);
   if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", b->mesh->device);
   const size_t N = size_t(n), C = size_t(b->cap);
-  cudaError_t e = cudaSuccess;
+  cudaError_t e = ensure_backward(b);
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_gfd");
   auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   cudaStream_t st = b->streams[0];
   const int32_t want_steps = max_steps > 0 ? max_steps : default_max_steps(b->mesh->nf);

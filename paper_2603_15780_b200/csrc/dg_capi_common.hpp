@@ -53,10 +53,6 @@ struct dg_mesh {
   // contiguous shards of equal expected work, one per device, and run concurrently (dg_capi_multi.cu); results land
   // at the request index. A replica has no replicas of its own.
   std::vector<dg_mesh*> replicas;
-  // ring of {queue_head, total_crossings} pairs so that concurrent calls never share a cursor
-  static constexpr unsigned kRing = 256;
-  unsigned long long* counters = nullptr;
-  mutable std::atomic<unsigned> ring{0};
 
   dg::MeshView view() const {
     return dg::MeshView{rec, he, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
@@ -71,7 +67,6 @@ struct dg_mesh {
     for (int i = 0; i < 128; ++i) p.he_map[i] = he_map[i];
     p.he_map_ok = he_map_ok ? 1 : 0;
   }
-  unsigned long long* next_counters() const { return counters + 2 * (ring.fetch_add(1) % kRing); }
 };
 
 namespace dgapi {
@@ -85,6 +80,13 @@ int fail_cuda(cudaError_t e, const char* where);
     cudaError_t e__ = (expr);                                  \
     if (e__ != cudaSuccess) return dgapi::fail_cuda(e__, #expr); \
   } while (0)
+
+// The library's OWN stream-ordered memory pool of a device (staging buffers, GFD scratch, peer copies): freed
+// blocks stay cached in it between calls (release threshold = keep everything), and the process-wide default pool
+// of the device -- which other frameworks in the process allocate from -- is never touched. dg_trim() empties it.
+cudaMemPool_t staging_pool(int device);
+// cudaMallocAsync from that pool (the current device's)
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t stream);
 
 // Makes the mesh's device current for the scope of a call.
 struct DeviceGuard {
@@ -147,7 +149,7 @@ class Stage {
   struct Back { void* dev; void* host; size_t bytes; };
   void* alloc(size_t bytes) {
     void* d = nullptr;
-    cudaError_t e = cudaMallocAsync(&d, bytes ? bytes : 1, stream_);
+    cudaError_t e = pool_alloc(&d, bytes ? bytes : 1, stream_);
     if (e != cudaSuccess) { note(e); return nullptr; }
     allocs_.push_back(d);
     return d;
@@ -231,7 +233,7 @@ class PeerStage {
   struct Back { void* local; void* home; size_t bytes; };
   void* alloc(size_t bytes) {
     void* d = nullptr;
-    cudaError_t e = cudaMallocAsync(&d, bytes ? bytes : 1, stream_);
+    cudaError_t e = pool_alloc(&d, bytes ? bytes : 1, stream_);
     if (e != cudaSuccess) { note(e); return nullptr; }
     allocs_.push_back(d);
     return d;

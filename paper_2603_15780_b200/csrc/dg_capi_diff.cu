@@ -25,8 +25,8 @@ struct AuxOut {
 
 cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const double* jb, const double* jd,
                      const double* jp, int32_t* rf, double* rb, double* rd, double* rp, uint8_t* rt, uint8_t* rs,
-                     int max_steps, unsigned long long* total, cudaStream_t stream, int siblings = 0,
-                     int64_t sibling_stride = 0, const AuxOut* aux = nullptr) {
+                     int max_steps, unsigned long long* total, cudaStream_t stream, unsigned long long* cursor,
+                     int siblings = 0, int64_t sibling_stride = 0, const AuxOut* aux = nullptr) {
   if (n <= 0) return cudaSuccess;
   dg::TraceParams p{};
   mesh->bind(p);
@@ -41,11 +41,8 @@ cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const do
     p.o_traced = aux->traced; p.o_requested = aux->requested; p.o_stall = aux->stall;
     p.o_npoints = aux->npoints; p.o_crossings = aux->crossings;
   }
-  unsigned long long* ctr = mesh->next_counters();
-  p.queue_head = ctr;
+  p.queue_head = cursor;   // zeroed by the caller (one word per launch of the call, from its own staging)
   p.total_crossings = total;
-  cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), stream);
-  if (e != cudaSuccess) return e;
   return dg::launch_trace(p, false, jp != nullptr, dg::LaunchShape{mesh->sm_count, 0}, stream);
 }
 
@@ -450,6 +447,8 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
     b.par_face = par_rface; b.par_bary = par_rbary; b.par_term = par_rterm; b.par_status = par_rstatus;
   }
   b.err = st.scratch<unsigned long long>(8);
+  unsigned long long* cursors = st.scratch<unsigned long long>(8);   // one work cursor per trace launch of this call
+  if (cursors) st.note(cudaMemsetAsync(cursors, 0, 8 * sizeof(unsigned long long), stream));
   // fused forward (dg_trace_gfd): the base jobs [3n, 4n) of round 2 write the rest of the forward result record
   AuxOut aux;
   unsigned long long* fwd_total = nullptr;
@@ -470,19 +469,19 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   // round 1: the two payload-carrying eps-length seeds of every sample
   st.note(dg::launch_gfd_round1_jobs(b, stream));
   st.note(run_jobs(mesh, 2 * n, b.j1_face, b.j1_bary, b.j1_dir, b.j1_payload, b.r1_face, b.r1_bary, b.r1_dir,
-                   b.r1_payload, b.r1_term, b.r1_status, max_steps, nullptr, stream));
+                   b.r1_payload, b.r1_term, b.r1_status, max_steps, nullptr, stream, cursors + 0));
   // round 2: the full-length jobs of every sample as one sibling group
   st.note(dg::launch_gfd_round2_jobs(b, stream));
   const int group = c.schedule == DG_GFD_SCHEDULE_PLAIN ? 0 : gfd_siblings();
   if (known_base) {
     st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, nullptr, nullptr,
-                     b.r2_term, b.r2_status, max_steps, nullptr, stream, group ? 3 : 0, n));
+                     b.r2_term, b.r2_status, max_steps, nullptr, stream, cursors + 1, group ? 3 : 0, n));
   } else {
     st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, r2_dir, nullptr,
-                     b.r2_term, b.r2_status, max_steps, fwd_total, stream, group ? 4 : 0, n, fwd ? &aux : nullptr));
+                     b.r2_term, b.r2_status, max_steps, fwd_total, stream, cursors + 1, group ? 4 : 0, n, fwd ? &aux : nullptr));
     st.note(dg::launch_gfd_par_jobs(b, stream));
     st.note(run_jobs(mesh, n, b.par_jface, b.par_jbary, b.par_jdir, nullptr, par_rface, par_rbary, nullptr, nullptr,
-                     par_rterm, par_rstatus, max_steps, nullptr, stream));
+                     par_rterm, par_rstatus, max_steps, nullptr, stream, cursors + 2));
   }
   st.note(dg::launch_gfd_assemble(b, stream));
   st.note(cudaMemcpyAsync(h_err, b.err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
@@ -503,10 +502,10 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
     if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_gfd_jacobians fallback staging");
     st.note(dg::launch_gfd_fallback_jobs(b, stream));
     st.note(run_jobs(mesh, 4 * n, b.j3_face, b.j3_bary, b.j3_dir, b.j3_payload, b.r3_face, b.r3_bary, nullptr,
-                     b.r3_payload, b.r3_term, b.r3_status, max_steps, nullptr, stream));
+                     b.r3_payload, b.r3_term, b.r3_status, max_steps, nullptr, stream, cursors + 3));
     st.note(dg::launch_gfd_fallback_round2_jobs(b, stream));
     st.note(run_jobs(mesh, 2 * n, b.j4_face, b.j4_bary, b.j4_dir, nullptr, b.r4_face, b.r4_bary, nullptr, nullptr,
-                     b.r4_term, b.r4_status, max_steps, nullptr, stream));
+                     b.r4_term, b.r4_status, max_steps, nullptr, stream, cursors + 4));
     st.note(dg::launch_gfd_fallback_assemble(b, stream));
     st.note(cudaMemcpyAsync(h_err, b.err, sizeof h_err, cudaMemcpyDeviceToHost, stream));
     st.note(cudaStreamSynchronize(stream));

@@ -7,11 +7,41 @@
 // not depend on the schedule, and a shard's outputs are written at its own offsets of the caller's arrays.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <thread>
 
 #include "dg_capi_common.hpp"
 
 namespace dgapi {
+
+cudaMemPool_t staging_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    unsigned long long keep = ~0ull;   // a DG_MEM_HOST call must not pay for physical allocation every time
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[device] = pool;
+  }
+  return pools[device];
+}
+
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t stream) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool = staging_pool(dev);
+  if (!pool) return cudaMallocAsync(p, bytes, stream);   // (pool creation failed: the default pool, untouched)
+  return cudaMallocFromPoolAsync(p, bytes, pool, stream);
+}
 
 bool fan_out(const dg_mesh* mesh, int64_t n) {
   if (!mesh || mesh->replicas.empty()) return false;
