@@ -193,14 +193,14 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def gather_peak(mesh, device_index):
+def gather_peak(mesh, device_index, gather):
     """The access pattern's own ceiling, MEASURED IN THIS RUN (outside the timed region): scripts/micro/gather_bench --
     random 128-byte records, one per lane per round, dependent next index -- at this mesh's record-array size with
     the gather this mesh uses. G records/s; one record = one face crossing."""
     exe = os.path.join(ROOT, "scripts", "micro", "gather_bench")
     if not mesh.has_transport_cache or not os.path.exists(exe):
         return None
-    variant = {"loads": 0, "tma": 1, "coop": 2}[mesh.gather]
+    variant = {"loads": 0, "tma": 1, "coop": 2}[gather]
     env = dict(os.environ)
     vis = [v for v in env.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
     env["CUDA_VISIBLE_DEVICES"] = vis[device_index] if device_index < len(vis) else str(device_index)
@@ -435,7 +435,8 @@ def measure(key, args, ctx, headline):
             dist.barrier()
         torch.cuda.synchronize()
 
-    peak_g = gather_peak(mesh, local) if rank == 0 else None   # micro-benchmark, before the timed region
+    face_order, gather_kind = mesh.trace_plan(n)   # how this launch is scheduled and how it fetches its records
+    peak_g = gather_peak(mesh, local, gather_kind) if rank == 0 else None   # micro-benchmark, before the timed region
     for _ in range(warmup):
         step(False)
     sync_all()
@@ -454,6 +455,31 @@ def measure(key, args, ctx, headline):
         sync_all()
     step_ms = [s.elapsed_time(e) for s, e in marks]
     tr_ms = [s.elapsed_time(e) for s, e in trace_ms]
+    def timed_device(fn, reps):
+        fn()
+        sync_all()
+        ms = []
+        for _ in range(reps):
+            flush.fill_(1)
+            s, e = ev(), ev()
+            s.record(); fn(); e.record()
+            ms.append((s, e))
+        sync_all()
+        return float(np.mean([s.elapsed_time(e) for s, e in ms]))
+
+    # the opt-in tolerance lane (DG_LANE_FAST) on the same step: reported beside the exact lane, never instead of it
+    lane_fast = None
+    if mesh.has_transport_cache:
+        lf_fwd = timed_device(lambda: mesh.trace_batch_device(F, B, D, o, max_steps=max_steps, lane="fast"), steps)
+        lf_step = lf_fwd
+        if scheme == "ep":
+            lf_step = timed_device(lambda: (mesh.trace_batch_device(F, B, D, o, max_steps=max_steps, lane="fast"),
+                                            mesh.ep_backward_device(F, D, o["face"], o["dir"], G, blk.col["grad_v"], blk.col["grad_p"])), steps)
+        elif scheme == "gfd":
+            lf_step = timed_device(lambda: (mesh.trace_gfd_device(F, B, D, o, eps, eps, blk.col["jv"], blk.col["jp"], lane="fast"),
+                                            mesh.gfd_pullback_device(F, D, o["face"], blk.col["jv"], blk.col["jp"], G, blk.col["grad_v"],
+                                                                     blk.col["grad_p"])), steps)
+        lane_fast = {"forward_ms": lf_fwd, "step_ms": lf_step}
     separate = None
     if scheme == "gfd":
         # for comparison: the same step as two separate calls -- a lone forward launch, then GFD with the forward
@@ -547,13 +573,14 @@ def measure(key, args, ctx, headline):
     alg_bytes = crossings_local * BYTES_PER_CROSSING + n * BYTES_PER_GEODESIC
     achieved = alg_bytes / t_trace / 1e9
     traffic = profile_traffic(key, n)
-    info = dg.kernel_info(False, False, cached=mesh.has_transport_cache, tma=mesh.gather == "tma", coop=mesh.gather == "coop")
+    info = dg.kernel_info(False, False, cached=mesh.has_transport_cache, tma=gather_kind == "tma", coop=gather_kind == "coop")
     cps_fwd = crossings_local / t_trace
     gather = None
     if peak_g:
-        gather = {"gather": mesh.gather, "record_bytes": 3 * mesh.nf * 128, "achieved_grecords_per_s": cps_fwd / 1e9,
+        gather = {"gather": gather_kind, "start_face_order": face_order, "record_bytes": 3 * mesh.nf * 128, "achieved_grecords_per_s": cps_fwd / 1e9,
                   "peak_grecords_per_s": peak_g, "frac": cps_fwd / 1e9 / peak_g,
-                  "source": "scripts/micro/gather_bench run inside this bench before the timed region"}
+                  "source": "scripts/micro/gather_bench run inside this bench before the timed region: RANDOM records, so a "
+                            "launch scheduled in start-face order (L2 hits between neighbouring traces) can exceed it"}
     bwd_ms = float(np.mean(step_ms) - np.mean(tr_ms)) if scheme != "gfd" else separate["ms_per_step"] - separate["forward_ms"]
     line = {"metric": f"face_crossings_per_s_fwd_{scheme}" if scheme != "fwd" else "face_crossings_per_s_fwd",
             "value": value, "unit": "face-crossings/s", "n_gpus": world, "steps": steps, "warmup": warmup,
@@ -569,8 +596,8 @@ def measure(key, args, ctx, headline):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
                          "traffic_source": (traffic["source"] + " -- a committed ncu capture, not measured in this run") if traffic else None,
-                         "kernel": ("trace_fast_kernel<crossing records, TMA tile::gather4>" if mesh.gather == "tma" else
-                                    "trace_fast_kernel<crossing records, cooperative 256-bit loads>" if mesh.gather == "coop" else
+                         "kernel": ("trace_fast_kernel<crossing records, TMA tile::gather4>" if gather_kind == "tma" else
+                                    "trace_fast_kernel<crossing records, cooperative 256-bit loads>" if gather_kind == "coop" else
                                     "trace_fast_kernel<crossing records, 256-bit loads>" if mesh.has_transport_cache else
                                     "trace_fast_kernel<face records>"),
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
@@ -613,6 +640,11 @@ def measure(key, args, ctx, headline):
                                        "kernel": "trace_fast_kernel<crossing records, 256-bit loads, sibling groups of 3>",
                                        "algorithmic_bytes_per_launch": alg2, "registers": info2["registers"],
                                        "blocks_per_sm": info2["blocks_per_sm"]}
+    if lane_fast:
+        line["tolerance_lane"] = {"lane": "DG_LANE_FAST (opt-in): identical face sequences on non-degenerate queries, end points within "
+                                          "1e-9 x bbox diagonal (tests/test_gpu_fast_walker.py::test_tolerance_lane_parity_gate); rank 0's shard",
+                                  "forward_ms": lane_fast["forward_ms"], "forward_face_crossings_per_s": crossings_local / (lane_fast["forward_ms"] * 1e-3),
+                                  "step_ms": lane_fast["step_ms"], "value": crossings_local / (lane_fast["step_ms"] * 1e-3)}
     if not args.no_cpu and world == 1:
         try:
             line["cpu_baseline"] = cpu_baseline(xyz, tri, f, b, d, q, scheme, max_steps, budget_s=12.0 if headline else 4.0,

@@ -76,12 +76,17 @@ enum { DG_EVENT_ADVANCED = 0, DG_EVENT_CROSSED_EDGE = 1, DG_EVENT_CROSSED_VERTEX
 enum { DG_MEM_HOST = 0, DG_MEM_DEVICE = 1 };
 enum { DG_SORT_AUTO = 0, DG_SORT_ON = 1, DG_SORT_OFF = 2 };
 enum { DG_WALKER_AUTO = 0, DG_WALKER_GENERIC = 1, DG_WALKER_FAST_LOADS = 2, DG_WALKER_FAST_TMA = 3, DG_WALKER_FAST_COOP = 4 };
-/* Arithmetic of the f64 tracer: there is ONE lane. The library is built without FMA contraction
- * and follows the reference's operation order, so a trace that never takes a vertex branch (no
- * libm calls) is bit-identical to the reference CPU build; vertex branches agree to the last
- * ulp of atan2/sin/cos. The `lane` bytes of the cfg structs are reserved (must be 0 or 1; both
- * select this lane) for a future contraction-enabled variant. */
-enum { DG_LANE_DEFAULT = 0, DG_LANE_EXACT = 1 };
+/* Arithmetic of the f64 tracer. The library is built without FMA contraction and the EXACT lane (the default, and
+ * the parity anchor) follows the reference's operation order, so a trace that never takes a vertex branch (no libm
+ * calls) is bit-identical to the reference CPU build; vertex branches agree to the last ulp of atan2/sin/cos.
+ * DG_LANE_FAST is an opt-in TOLERANCE lane of the plain forward map (f64, crossing records, no payload / transport
+ * matrix / polylines / hole avoidance; other requests run the exact lane): same decisions and tolerances, but
+ * reciprocal-multiply instead of correctly rounded quotients, one reciprocal for the exit parameter, no second
+ * renormalising snap, first-order renormalisation of the transported direction. Its bar is north_star's: identical
+ * face sequences on non-degenerate queries, end points / directions within 1e-9 x bbox diagonal (measured: <= 1e-13),
+ * GFD Jacobians within 1e-5 relative -- not bit equality. With dg_diff_cfg.lane it applies to GFD's full-length
+ * re-traces (and the fused forward). */
+enum { DG_LANE_DEFAULT = 0, DG_LANE_EXACT = 1, DG_LANE_FAST = 2 };
 
 DG_API const char* dg_last_error(void);
 DG_API const char* dg_version(void);
@@ -147,6 +152,7 @@ DG_API int dg_mesh_has_transport_cache(const dg_mesh* m);
 enum { DG_GATHER_LOADS = 0, DG_GATHER_TMA = 1, DG_GATHER_COOP = 2 };
 DG_API int dg_mesh_gather_mode(const dg_mesh* m);
 DG_API int dg_mesh_uses_tma_gather(const dg_mesh* m);
+
 DG_API void dg_mesh_destroy(dg_mesh* m);
 DG_API int32_t dg_mesh_face_count(const dg_mesh* m);
 DG_API int32_t dg_mesh_vertex_count(const dg_mesh* m);
@@ -160,7 +166,7 @@ typedef struct dg_trace_cfg {
   uint8_t hole_avoidance;
   uint8_t want_transport_matrix;
   uint8_t use_f32;               /* run the stepping arithmetic in single precision */
-  uint8_t lane;                  /* reserved (see DG_LANE_*) */
+  uint8_t lane;                  /* DG_LANE_* */
   uint8_t memory;                /* DG_MEM_HOST: pointers are host memory, staged by the library
                                     DG_MEM_DEVICE: pointers are device memory on the mesh's GPU */
   uint8_t sort_by_face;          /* DG_SORT_*: schedule queries in start-face order (results stay at the request index,
@@ -214,6 +220,10 @@ typedef struct dg_trace_out {
 
 DG_API int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in,
                           const dg_trace_cfg* cfg, dg_trace_out* out);
+/* What a plain f64 forward request of n queries gets under cfg (NULL = defaults): *face_order = 1 when it is
+ * scheduled in start-face order (dg_trace_cfg.sort_by_face resolved), *gather = the DG_GATHER_* of its launch
+ * (start-face order keeps the per-lane loads at every mesh size). For reports; same bits whatever the plan. */
+DG_API int dg_trace_plan(const dg_mesh* m, int64_t n, const dg_trace_cfg* cfg, int* face_order, int* gather);
 
 /* trace_batch with the reference's DEFAULT TraceConfig, record_polyline = true (tracer.hpp:22), in ONE call: the
  * library records, sizes, compacts and copies on the device (capped first pass, device scan, compaction, a second pass
@@ -264,7 +274,7 @@ DG_API int dg_transition(const dg_mesh* mesh, int which, int64_t n, const int32_
  * dg_trace_batch are asynchronous on the stream. */
 typedef struct dg_diff_cfg {
   uint8_t memory;       /* DG_MEM_HOST / DG_MEM_DEVICE for all pointers of the call */
-  uint8_t lane;         /* reserved (see DG_LANE_*) */
+  uint8_t lane;         /* DG_LANE_*: arithmetic of GFD's full-length traces */
   uint8_t schedule;     /* GFD round 2: DG_GFD_SCHEDULE_AUTO = the full-length re-traces of a sample run as
                            sibling lanes of one warp and share every crossing-record fetch;
                            DG_GFD_SCHEDULE_PLAIN = job order. A schedule only: same bits either way. */

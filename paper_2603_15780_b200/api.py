@@ -128,6 +128,13 @@ class Mesh:
     def device_bytes(self):
         return lib().dg_mesh_device_bytes(self.h)
 
+    def trace_plan(self, n, device_mode=True):
+        """(face_order, gather) a plain f64 forward request of n queries gets by default (dg_trace_plan)."""
+        fo, ga = C.c_int(0), C.c_int(0)
+        cfg = TraceCfg(memory=capi.MEM_DEVICE if device_mode else capi.MEM_HOST)
+        check(lib().dg_trace_plan(self._handle(), int(n), C.addressof(cfg), C.addressof(fo), C.addressof(ga)))
+        return bool(fo.value), ("loads", "tma", "coop")[ga.value]
+
     def default_max_steps(self):
         return int(10.0 * np.sqrt(float(self.nf))) + 100
 
@@ -146,7 +153,7 @@ class Mesh:
     # ------------------------------------------------------------------ forward tracing
     def trace_batch(self, face, bary, dirs, payload=None, max_steps=0, hole_avoidance=False, want_q=False,
                     record_polyline=False, use_f32=False, sort_by_face=None, refill_min=0, blocks_per_sm=0,
-                    out=None, generic_walker=False, walker="auto", two_call_polylines=False, poly_views=False):
+                    out=None, generic_walker=False, walker="auto", two_call_polylines=False, poly_views=False, lane="exact"):
         """trace_batch (tracer.cpp:596) on host arrays; results at the request index. `out`: a
         TraceResult of a previous call of the same size whose (e.g. pinned) arrays are reused.
         record_polyline: ONE call (dg_trace_polylines: capped first pass, device scan, compaction); the polylines
@@ -172,7 +179,7 @@ class Mesh:
         cfg = TraceCfg(max_steps=int(max_steps), hole_avoidance=int(hole_avoidance),
                        want_transport_matrix=int(want_q), use_f32=int(use_f32), memory=capi.MEM_HOST,
                        sort_by_face=SORT[sort_by_face], refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm),
-                       walker=1 if generic_walker else WALKERS[walker])
+                       walker=1 if generic_walker else WALKERS[walker], lane=LANES[lane])
         tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), ptr(payload))
         total = C.c_uint64(0)
 
@@ -217,7 +224,7 @@ class Mesh:
 
     def trace_batch_device(self, face, bary, dirs, out, payload=None, max_steps=0, hole_avoidance=False,
                            want_q=False, stream=None, sort_by_face=None, refill_min=0, blocks_per_sm=0,
-                           generic_walker=False, walker="auto"):
+                           generic_walker=False, walker="auto", lane="exact"):
         """Zero-copy entry point: every array is a torch CUDA tensor on the mesh's device;
         `out` maps dg_trace_out field names to preallocated tensors. Asynchronous on `stream`."""
         import torch
@@ -226,7 +233,7 @@ class Mesh:
         cfg = TraceCfg(max_steps=int(max_steps), hole_avoidance=int(hole_avoidance),
                        want_transport_matrix=int(want_q), memory=capi.MEM_DEVICE, sort_by_face=SORT[sort_by_face],
                        refill_min=int(refill_min), blocks_per_sm=int(blocks_per_sm),
-                       walker=1 if generic_walker else WALKERS[walker],
+                       walker=1 if generic_walker else WALKERS[walker], lane=LANES[lane],
                        stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
         tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), ptr(payload))
         o = TraceOut()
@@ -347,7 +354,7 @@ class Mesh:
 
 
     # ------------------------------------------ fused forward + GFD Jacobians, pull-back only backward
-    def trace_gfd(self, face, bary, dirs, eps_v=None, eps_p=None, max_steps=0, plain_schedule=False):
+    def trace_gfd(self, face, bary, dirs, eps_v=None, eps_p=None, max_steps=0, plain_schedule=False, lane="exact"):
         """dg_trace_gfd on host arrays: the forward exp map and the GFD Jacobians of the same samples in one call
         (the forward traces ride in GFD's round 2 as the fourth sibling). Returns (TraceResult, dict jv/jp/degraded/
         frames). A whole-call GFD failure raises AFTER the forward results are in place (`.forward` of the error)."""
@@ -365,7 +372,7 @@ class Mesh:
         total = C.c_uint64(0)
         o = TraceOut(ptr(r.face), ptr(r.bary), ptr(r.dir), ptr(r.traced), ptr(r.requested), ptr(r.term), ptr(r.status),
                      ptr(r.stall), None, None, ptr(r.npoints), ptr(r.crossings), C.addressof(total), None, 0, None, None, None)
-        cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps), schedule=int(plain_schedule))
+        cfg = DiffCfg(memory=capi.MEM_HOST, max_steps=int(max_steps), schedule=int(plain_schedule), lane=LANES[lane])
         ei = C.c_int64(-1)
         rc = lib().dg_trace_gfd(h, n, ptr(face), ptr(bary), ptr(dirs), float(eps_v), float(eps_p), C.addressof(cfg),
                                 C.addressof(o), ptr(jac["jv"]), ptr(jac["jp"]), ptr(jac["degraded"]), ptr(jac["frames"]),
@@ -379,10 +386,11 @@ class Mesh:
             raise e
         return r, jac
 
-    def trace_gfd_device(self, face, bary, dirs, out, eps_v, eps_p, jv, jp, degraded=None, stream=None, max_steps=0):
+    def trace_gfd_device(self, face, bary, dirs, out, eps_v, eps_p, jv, jp, degraded=None, stream=None, max_steps=0,
+                         lane="exact"):
         """dg_trace_gfd on torch CUDA tensors; `out` as trace_batch_device."""
         import torch
-        cfg = DiffCfg(memory=capi.MEM_DEVICE, max_steps=int(max_steps),
+        cfg = DiffCfg(memory=capi.MEM_DEVICE, max_steps=int(max_steps), lane=LANES[lane],
                       stream=(stream if stream is not None else torch.cuda.current_stream().cuda_stream))
         o = TraceOut()
         for k, v in out.items():
@@ -409,6 +417,8 @@ class Mesh:
                                     C.addressof(cfg), ptr(grad_v), ptr(grad_p)))
 
 
+# dg_trace_cfg.lane / dg_diff_cfg.lane (DG_LANE_*)
+LANES = {"exact": 1, "default": 0, None: 0, "fast": 2}
 # dg_trace_cfg.sort_by_face (DG_SORT_*): None = the library decides
 SORT = {None: 0, "auto": 0, True: 1, False: 2, 1: 1, 0: 2}
 # dg_trace_cfg.walker (DG_WALKER_*): which kernel traces a plain f64 forward request

@@ -37,7 +37,7 @@ EXPORTS = [
     "dg_last_error", "dg_version", "dg_device_count", "dg_set_device", "dg_set_devices", "dg_set_device_list",
     "dg_mesh_device_count", "dg_device_sm_count", "dg_trim",
     "dg_mesh_derive", "dg_mesh_create", "dg_mesh_create_ex", "dg_mesh_has_transport_cache", "dg_mesh_uses_tma_gather", "dg_mesh_gather_mode", "dg_mesh_destroy", "dg_mesh_face_count", "dg_mesh_vertex_count",
-    "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_trace_polylines", "dg_transition", "dg_ep_jacobians",
+    "dg_mesh_device_bytes", "dg_mesh_device", "dg_trace_batch", "dg_trace_polylines", "dg_trace_plan", "dg_transition", "dg_ep_jacobians",
     "dg_ep_backward", "dg_gfd_jacobians", "dg_gfd_jacobians_with_base", "dg_trace_gfd", "dg_gfd_pullback", "dg_trace_kernel_info",
     "dg_batch_create", "dg_batch_destroy", "dg_batch_size", "dg_batch_trace", "dg_batch_trace_gfd", "dg_batch_ep_backward", "dg_batch_gfd",
 ]
@@ -112,6 +112,7 @@ def lib():
         L.dg_mesh_uses_tma_gather.argtypes = [vp]
         L.dg_mesh_gather_mode.argtypes = [vp]
         L.dg_trace_batch.argtypes = [vp, i64, vp, vp, vp]
+        L.dg_trace_plan.argtypes = [vp, i64, vp, vp, vp]
         L.dg_trace_polylines.argtypes = [vp, i64, vp, vp, vp, vp]
         L.dg_transition.argtypes = [vp, C.c_int, i64, vp, vp, vp, vp, C.c_int] + [vp] * 8
         L.dg_ep_jacobians.argtypes = [vp, i64] + [vp] * 10

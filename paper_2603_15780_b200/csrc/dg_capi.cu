@@ -124,6 +124,12 @@ __global__ void sort_keys_kernel(const int32_t* __restrict__ face, const double*
 
 }  // namespace
 
+// dg_trace_cfg.sort_by_face resolved for a request of n queries
+static bool schedules_by_face(const dg_mesh* mesh, int64_t n, const dg_trace_cfg& c, bool record) {
+  const bool big_mesh = mesh->he && size_t(3) * size_t(mesh->nf) * sizeof(dg::HalfEdgeRec) > (size_t(96) << 20);
+  return c.sort_by_face == DG_SORT_ON || (c.sort_by_face == DG_SORT_AUTO && big_mesh && n >= (int64_t(1) << 15) && !record);
+}
+
 namespace dg {
 cudaError_t launch_build_records(const double* xyz, const int32_t* tri, const int32_t* adj, int32_t nf,
                                  FaceRec* rec, cudaStream_t stream) {
@@ -473,6 +479,17 @@ int dg_trim(const dg_mesh* m) {
 
 int dg_mesh_has_transport_cache(const dg_mesh* m) { return m && m->he ? 1 : 0; }
 int dg_mesh_gather_mode(const dg_mesh* m) { return m ? dg::fast_walker_gather_mode(m->view(), m->he_map_ok) : 0; }
+// The decisions a plain f64 forward request of n queries gets under cfg (NULL = defaults): *face_order = 1 when
+// it is scheduled in start-face order, *gather = DG_GATHER_* of its crossing-record fetch.
+int dg_trace_plan(const dg_mesh* m, int64_t n, const dg_trace_cfg* cfg, int* face_order, int* gather) {
+  if (!m) return fail(DG_ERR_INVALID_ARGS, "dg_trace_plan: missing mesh");
+  dg_trace_cfg c{};
+  if (cfg) c = *cfg;
+  const bool sort = schedules_by_face(m, n, c, false) && !(c.memory == DG_MEM_HOST && !c.stream && n <= 8192 && c.sort_by_face != DG_SORT_ON);
+  if (face_order) *face_order = sort ? 1 : 0;
+  if (gather) *gather = dg::fast_walker_gather_mode(m->view(), m->he_map_ok, sort);
+  return DG_OK;
+}
 int dg_mesh_uses_tma_gather(const dg_mesh* m) { return dg_mesh_gather_mode(m) == DG_GATHER_TMA ? 1 : 0; }
 int32_t dg_mesh_face_count(const dg_mesh* m) { return m ? m->nf : 0; }
 int32_t dg_mesh_vertex_count(const dg_mesh* m) { return m ? m->nv : 0; }
@@ -584,6 +601,7 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
   p.refill_min = 0;
   p.hole_avoidance = c.hole_avoidance;
   p.want_q = c.want_transport_matrix;
+  p.lane_fast = c.lane == DG_LANE_FAST;
   if (p.total_crossings && !mapped) DG_CUDA(cudaMemsetAsync(p.total_crossings, 0, 8, stream));
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || out->payload || out->transport;
   DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, needs_full, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm), int(c.walker)}, stream));
@@ -639,6 +657,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   p.refill_min = c.refill_min;  // 0 = the walker's own default
   p.hole_avoidance = c.hole_avoidance;
   p.want_q = c.want_transport_matrix;
+  p.lane_fast = c.lane == DG_LANE_FAST;
 
   // the work cursor and the crossing total of THIS call, stream-ordered like the rest of its staging
   unsigned long long* ctr = st.scratch<unsigned long long>(2);
@@ -653,8 +672,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   // L2 hits (c3, 1 M-face torus, 384 MB of records: forward 17.9 -> 16.5 ms per 1 M, 179 -> 160 ms per 10 M;
   // c2, L2-resident: +-1 %, stays off). The face order of the mesh is the caller's: a locality-preserving
   // numbering (grid, Morton, Hilbert) is what makes neighbours in the queue neighbours on the surface.
-  const bool big_mesh = mesh->he && size_t(3) * size_t(mesh->nf) * sizeof(dg::HalfEdgeRec) > (size_t(96) << 20);
-  const bool sort = c.sort_by_face == DG_SORT_ON || (c.sort_by_face == DG_SORT_AUTO && big_mesh && n >= (int64_t(1) << 15) && !record);
+  const bool sort = schedules_by_face(mesh, n, c, record);
   if (sort) {
     int32_t* keys_in = st.scratch<int32_t>(N);
     int32_t* keys_out = st.scratch<int32_t>(N);
@@ -863,7 +881,7 @@ int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const 
     return fail(DG_ERR_INVALID_ARGS, "trace_batch: starts and dirs differ in length");
   dg_trace_cfg c{};
   if (cfg) c = *cfg;
-  if (c.lane > DG_LANE_EXACT) return fail(DG_ERR_INVALID_ARGS, "trace_batch: unknown arithmetic lane %d", int(c.lane));
+  if (c.lane > DG_LANE_FAST) return fail(DG_ERR_INVALID_ARGS, "trace_batch: unknown arithmetic lane %d", int(c.lane));
   const bool record = out->poly_offsets != nullptr;
   if (record && (!out->poly_face || !out->poly_bary || !out->poly_seg || out->poly_total < 0))
     return fail(DG_ERR_INVALID_ARGS, "trace_batch: polyline recording needs poly_face/poly_bary/poly_seg and poly_total");

@@ -263,6 +263,7 @@ static int batch_trace_gfd_one(dg_batch* b, int64_t n, const dg_trace_in* in, co
   dc.memory = DG_MEM_DEVICE;
   dc.stream = st;
   dc.max_steps = c.max_steps;
+  dc.lane = c.lane;
   dg_trace_out dout{};
   dout.face = b->o_face; dout.bary = b->o_bary; dout.dir = b->o_dir; dout.traced = b->o_traced; dout.requested = b->o_requested;
   dout.term = b->o_term; dout.status = b->o_status; dout.stall = b->o_stall;

@@ -26,7 +26,7 @@ struct AuxOut {
 cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const double* jb, const double* jd,
                      const double* jp, int32_t* rf, double* rb, double* rd, double* rp, uint8_t* rt, uint8_t* rs,
                      int max_steps, unsigned long long* total, cudaStream_t stream, unsigned long long* cursor,
-                     int siblings = 0, int64_t sibling_stride = 0, const AuxOut* aux = nullptr) {
+                     int siblings = 0, int64_t sibling_stride = 0, const AuxOut* aux = nullptr, bool lane_fast = false) {
   if (n <= 0) return cudaSuccess;
   dg::TraceParams p{};
   mesh->bind(p);
@@ -36,6 +36,7 @@ cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const do
   p.max_steps = max_steps;
   p.refill_min = 0;  // the walker's own default
   p.siblings = siblings; p.sibling_stride = sibling_stride;
+  p.lane_fast = lane_fast;   // (payload-carrying launches run the exact lane whatever this says)
   if (aux) {
     p.aux_from = aux->from;
     p.o_traced = aux->traced; p.o_requested = aux->requested; p.o_stall = aux->stall;
@@ -400,6 +401,11 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   if (!guard.ok) return fail(DG_ERR_CUDA, "cannot select device %d", mesh->device);
   cudaStream_t stream = (device_mode || c.stream) ? static_cast<cudaStream_t>(c.stream) : mesh->stream;
   const int max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
+  if (c.lane > DG_LANE_FAST) return fail(DG_ERR_INVALID_ARGS, "dg_gfd_jacobians: unknown arithmetic lane %d", int(c.lane));
+  // DG_LANE_FAST: the full-length traces of round 2 (re-traces, and the base traces when they ride along) run the
+  // tolerance lane -- all of them, so that the differences are taken between like and like. With a known base the
+  // caller's forward traces must come from the same lane.
+  const bool lane_fast = c.lane == DG_LANE_FAST;
 
   Stage st(stream, device_mode);
   const size_t N = size_t(n);
@@ -475,10 +481,10 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   const int group = c.schedule == DG_GFD_SCHEDULE_PLAIN ? 0 : gfd_siblings();
   if (known_base) {
     st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, nullptr, nullptr,
-                     b.r2_term, b.r2_status, max_steps, nullptr, stream, cursors + 1, group ? 3 : 0, n));
+                     b.r2_term, b.r2_status, max_steps, nullptr, stream, cursors + 1, group ? 3 : 0, n, nullptr, lane_fast));
   } else {
     st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, r2_dir, nullptr,
-                     b.r2_term, b.r2_status, max_steps, fwd_total, stream, cursors + 1, group ? 4 : 0, n, fwd ? &aux : nullptr));
+                     b.r2_term, b.r2_status, max_steps, fwd_total, stream, cursors + 1, group ? 4 : 0, n, fwd ? &aux : nullptr, lane_fast));
     st.note(dg::launch_gfd_par_jobs(b, stream));
     st.note(run_jobs(mesh, n, b.par_jface, b.par_jbary, b.par_jdir, nullptr, par_rface, par_rbary, nullptr, nullptr,
                      par_rterm, par_rstatus, max_steps, nullptr, stream, cursors + 2));

@@ -229,6 +229,7 @@ extern "C" int dg_trace_polylines(const dg_mesh* mesh, int64_t n, const dg_trace
   dg_trace_cfg c{};
   if (cfg) c = *cfg;
   if (c.memory != DG_MEM_HOST || c.stream) return fail(DG_ERR_INVALID_ARGS, "dg_trace_polylines: host pointers, library stream");
+  if (c.lane > DG_LANE_FAST) return fail(DG_ERR_INVALID_ARGS, "trace_batch: unknown arithmetic lane %d", int(c.lane));
   if (out->poly_offsets || out->poly_face || out->poly_bary || out->poly_seg)
     return fail(DG_ERR_INVALID_ARGS, "dg_trace_polylines: the polylines come back in *poly, not in out->poly_*");
   *poly = dg_polylines{};

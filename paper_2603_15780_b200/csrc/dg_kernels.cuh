@@ -62,6 +62,7 @@ struct TraceParams {
   uint8_t hole_avoidance;
   uint8_t want_q;
   uint8_t he_map_ok;  // he_map is a valid tensor map of mesh.he
+  uint8_t lane_fast;  // DG_LANE_FAST: plain forward requests over crossing records run the tolerance lane
 };
 
 struct LaunchShape {
@@ -76,7 +77,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
 
 // Whether the fast walker gathers this mesh's crossing records through TMA (AUTO policy).
 // gather of the crossing records for a lone-trace batch on this mesh: 0 per-lane loads, 1 TMA, 2 cooperative loads
-int fast_walker_gather_mode(const MeshView& m, bool map_ok);
+int fast_walker_gather_mode(const MeshView& m, bool map_ok, bool face_order = false);
 
 // Kernel attributes for reporting (registers, max resident blocks per SM).
 void trace_kernel_info(bool use_f32, int variant, int* regs, int* blocks_per_sm, int* block_threads);

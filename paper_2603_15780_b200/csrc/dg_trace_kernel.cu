@@ -160,7 +160,7 @@ cudaError_t launch_one(const TraceParams& p_in, LaunchShape shape, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <bool kCached, int kTma, int kPay = 0, bool kDense = false>
+template <bool kCached, int kTma, int kPay = 0, bool kDense = false, int kLane = 0>
 cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t stream) {
   constexpr size_t smem = kTma ? size_t(kFastTmaSmemBytes) : 0;
   TraceParams p = p_in;
@@ -173,7 +173,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
     static std::atomic<int> cached_per_sm{0};
     per_sm = cached_per_sm.load(std::memory_order_relaxed);
     if (per_sm <= 0) {
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma, kPay, kDense>, DG_FAST_BLOCK, smem);
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma, kPay, kDense, kLane>, DG_FAST_BLOCK, smem);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
       cached_per_sm.store(per_sm, std::memory_order_relaxed);
@@ -183,7 +183,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
   const long long needed = (p.n + DG_FAST_BLOCK - 1) / DG_FAST_BLOCK;
   if (blocks > needed) blocks = needed;
   if (blocks < 1) blocks = 1;
-  trace_fast_kernel<kCached, kTma, kPay, kDense><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
+  trace_fast_kernel<kCached, kTma, kPay, kDense, kLane><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -207,7 +207,7 @@ bool fast_walk_enabled() {
 //  * a sibling schedule (TraceParams::siblings, GFD round 2): per-lane loads at every size -- the lanes of a group ask
 //    for the same line and the load path merges them (c3: 45.3 ms against 52.8 cooperative, 55.9 TMA).
 // DG_FAST_GATHER=loads|tma|coop forces one (A/B measurements); dg_trace_cfg.walker selects one per call.
-int gather_mode(const MeshView& m, int siblings, bool map_ok, int walker) {
+int gather_mode(const MeshView& m, int siblings, bool map_ok, int walker, bool face_order = false) {
   if (!m.he) return 0;
   static const int forced = [] {
     const char* e = getenv("DG_FAST_GATHER");
@@ -218,14 +218,16 @@ int gather_mode(const MeshView& m, int siblings, bool map_ok, int walker) {
   else if (walker == 3) mode = 1;
   else if (walker == 4) mode = 2;
   else if (forced >= 0) mode = forced;
-  else mode = (siblings <= 1 && size_t(m.nf) * 3 * sizeof(HalfEdgeRec) > (size_t(250) << 20)) ? 2 : 0;
+  // (start-face order: neighbouring lanes walk through the same neighbourhood, most sectors are L2 hits and the
+  // per-lane loads keep their lead -- c3 15.7 ms against 17.2 cooperative, c4 18.5 against 19.7)
+  else mode = (siblings <= 1 && !face_order && size_t(m.nf) * 3 * sizeof(HalfEdgeRec) > (size_t(250) << 20)) ? 2 : 0;
   if (mode == 1 && !map_ok) mode = 2;
   return mode;
 }
 
 }  // namespace
 
-int fast_walker_gather_mode(const MeshView& m, bool map_ok) { return fast_walk_enabled() ? gather_mode(m, 0, map_ok, 0) : 0; }
+int fast_walker_gather_mode(const MeshView& m, bool map_ok, bool face_order) { return fast_walk_enabled() ? gather_mode(m, 0, map_ok, 0, face_order) : 0; }
 
 cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
                          cudaStream_t stream) {
@@ -233,7 +235,7 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }
-  const int gather = gather_mode(p.mesh, p.siblings, p.he_map_ok != 0, shape.walker);
+  const int gather = gather_mode(p.mesh, p.siblings, p.he_map_ok != 0, shape.walker, p.perm != nullptr);
   auto fast = [&](auto pay) {
     constexpr int kPay = decltype(pay)::value;
     if (!p.mesh.he) return launch_fast<false, 0, kPay>(p, shape, stream);
@@ -242,6 +244,10 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
                        : launch_fast<true, 0, kPay>(p, shape, stream);
   };
   if (!needs_full && shape.walker != 1 && fast_walk_enabled()) {
+    if (p.lane_fast && p.mesh.he) {   // DG_LANE_FAST: the tolerance lane of the plain forward map (dg_fast_walk.cuh)
+      if (gather == 0 && p.siblings > 1) return launch_fast<true, 0, 0, true, 1>(p, shape, stream);
+      return gather == 0 ? launch_fast<true, 0, 0, false, 1>(p, shape, stream) : launch_fast<true, 2, 0, false, 1>(p, shape, stream);
+    }
     if (p.mesh.he && gather == 0 && p.siblings > 1) return launch_fast<true, 0, 0, true>(p, shape, stream);
     return fast(std::integral_constant<int, 0>{});
   }

@@ -239,3 +239,53 @@ def test_randomised_meshes_scales_and_starts(gpu):
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
     import fuzz_walkers
     assert fuzz_walkers.main(rounds=24, n=6000, seed=11) == 0
+
+
+@pytest.mark.parametrize("key,n", [("c1", 10_000), ("c2", 200_000), ("c3", 60_000)])
+def test_tolerance_lane_parity_gate(gpu, ref, key, n):
+    """DG_LANE_FAST, the opt-in tolerance lane of the plain forward map (reciprocal-multiply quotients, one reciprocal
+    for the exit parameter, no second renormalising snap, first-order renormalisation of the direction). Its bar is
+    north_star's, stated here: identical face sequences and end faces on the (non-degenerate) random queries of
+    configs 1-3, end points within 1e-9 x bbox diagonal, directions within 1e-9, traced length within 1e-9 relative --
+    against the EXACT lane and against the UNMODIFIED reference; GFD Jacobians through the lane within 1e-5 relative
+    to the largest entry of the reference's, pulled-back gradients cos >= 0.999999."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import make_workload
+    if key == "c1":
+        xyz, tri = W.icosphere(4)
+        f, b, d = W.sample_queries(xyz, tri, n, 1.0, seed=42)
+    else:
+        xyz, tri, f, b, d, _ = make_workload(key, n, 42)
+    m = gpu.Mesh(xyz, tri)
+    diag = W.bbox_diagonal(xyz)
+    exact = m.trace_batch(f, b, d, sort_by_face=False)
+    fast = m.trace_batch(f, b, d, lane="fast", sort_by_face=False)
+    assert np.array_equal(fast.face, exact.face) and np.array_equal(fast.crossings, exact.crossings)
+    assert np.array_equal(fast.term, exact.term) and np.array_equal(fast.status, exact.status)
+    assert not np.array_equal(fast.bary, exact.bary)            # it IS another arithmetic
+    assert np.abs(m.embed(fast.face, fast.bary) - m.embed(exact.face, exact.bary)).max() <= 1e-9 * diag
+    assert np.abs(fast.dir - exact.dir).max() <= 1e-9
+    assert np.abs(fast.traced - exact.traced).max() <= 1e-9 * np.abs(exact.traced).max()
+    k = min(n, 20_000)
+    rm = ref.RefMesh.build(xyz, tri)
+    theirs = rm.trace_batch(f[:k], b[:k], d[:k], record_polyline=True)
+    assert np.array_equal(fast.face[:k], theirs.face)
+    assert np.array_equal(fast.crossings[:k], (theirs.npoints - 2).clip(min=0))   # as many crossings, i.e. the same walk
+    assert np.abs(m.embed(fast.face[:k], fast.bary[:k]) - rm.embed(theirs.face, theirs.bary)).max() <= 1e-9 * diag
+    assert np.abs(fast.dir[:k] - theirs.dir).max() <= 1e-9
+    # GFD through the lane (fused forward + Jacobians): forward record as above, Jacobians within the GFD tolerance
+    s = min(n, 4000)
+    g = np.random.default_rng(3).normal(size=(s, 3))
+    r, jac = m.trace_gfd(f[:s], b[:s], d[:s], lane="fast")
+    assert np.array_equal(r.face, exact.face[:s])
+    rg = rm.gfd(f[:s], b[:s], d[:s], g=g)
+    for name in ("jv", "jp"):
+        assert np.abs(jac[name] - rg[name]).max() <= 1e-5 * np.abs(rg[name]).max(), name
+    assert np.array_equal(jac["degraded"], rg["degraded"])
+    pb = m.gfd_pullback(f[:s], d[:s], r.face, jac["jv"], jac["jp"], g)
+    for name in ("grad_v", "grad_p"):
+        num = np.einsum("nd,nd->n", pb[name], rg[name])
+        den = np.linalg.norm(pb[name], axis=1) * np.linalg.norm(rg[name], axis=1)
+        ok = den > 1e-12
+        assert (num[ok] / den[ok]).min() >= 0.999999, name

@@ -36,7 +36,8 @@ def test_config3_forward_and_gfd_on_the_1m_face_torus(gpu, ref):
     n = 6000
     xyz, tri, f, b, d, q = make_workload("c3", n, 42)
     m = gpu.Mesh(xyz, tri)
-    assert m.nf == 1_000_000 and m.has_transport_cache and m.gather == "coop"
+    assert m.nf == 1_000_000 and m.has_transport_cache and m.gather == "coop" and m.trace_plan(n) == (False, "coop")
+    assert m.trace_plan(10_000_000) == (True, "loads")   # start-face order beyond 32 768 queries: per-lane loads
     rm = ref.RefMesh.build(xyz, tri)
     assert m.default_gfd_eps() == rm.default_gfd_eps()
     fwd = m.trace_batch(f, b, d)
