@@ -193,22 +193,25 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def gather_peak(mesh, device_index, gather):
+def gather_peak(mesh, device_index):
     """The access pattern's own ceiling, MEASURED IN THIS RUN (outside the timed region): scripts/micro/gather_bench --
-    random 128-byte records, one per lane per round, dependent next index -- at this mesh's record-array size with
-    the gather this mesh uses. G records/s; one record = one face crossing."""
+    random 128-byte records, one per lane per round, dependent next index -- at this mesh's record-array size, the
+    best of the three gathers the walker has (per-lane 256-bit loads, TMA, cooperative loads). G records/s; one
+    record = one face crossing. Returns (peak, {variant: rate})."""
     exe = os.path.join(ROOT, "scripts", "micro", "gather_bench")
     if not mesh.has_transport_cache or not os.path.exists(exe):
-        return None
-    variant = {"loads": 0, "tma": 1, "coop": 2}[gather]
+        return None, None
     env = dict(os.environ)
     vis = [v for v in env.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
     env["CUDA_VISIBLE_DEVICES"] = vis[device_index] if device_index < len(vis) else str(device_index)
-    try:
-        out = subprocess.run([exe, str(3 * mesh.nf), "2000", str(variant)], env=env, capture_output=True, text=True, timeout=120)
-        return float(json.loads(out.stdout.strip().splitlines()[-1])["grecords_per_s"])
-    except Exception:
-        return None
+    rates = {}
+    for name, variant in (("loads", 0), ("tma", 1), ("coop", 2)):
+        try:
+            out = subprocess.run([exe, str(3 * mesh.nf), "1000", str(variant)], env=env, capture_output=True, text=True, timeout=120)
+            rates[name] = float(json.loads(out.stdout.strip().splitlines()[-1])["grecords_per_s"])
+        except Exception:
+            pass
+    return (max(rates.values()), rates) if rates else (None, None)
 
 
 def profile_traffic(key, n):
@@ -301,12 +304,11 @@ def run_reference_arm(args):
     t_ms = float(np.median(ms))
     v = crossings / (t_ms * 1e-3)
     cfg = config_of(key, n, len(tri), 1)
-    cfg["reference_sample"] = f"first {k} of {n} geodesics per step"
     line = {"impl": "reference", "metric": f"face_crossings_per_s_fwd_{wl['scheme']}", "value": v,
             "unit": "face-crossings/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_ms, "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": cfg, "geodesics_per_s": k / (t_ms * 1e-3),
-            "crossings_per_geodesic": crossings / k,
+            "crossings_per_geodesic": crossings / k, "reference_sample": f"first {k} of {n} geodesics per step",
             "cpu_baseline": {"value": v, "unit": "face-crossings/s", "cores": ref.threads, "kind": "reference",
                              "sample": f"first {k} of {n} geodesics, median of {args.steps} steps",
                              "note": "unmodified reference sources compiled into oracle/_ref, OpenMP over all host threads"},
@@ -436,7 +438,7 @@ def measure(key, args, ctx, headline):
         torch.cuda.synchronize()
 
     face_order, gather_kind = mesh.trace_plan(n)   # how this launch is scheduled and how it fetches its records
-    peak_g = gather_peak(mesh, local, gather_kind) if rank == 0 else None   # micro-benchmark, before the timed region
+    peak_g, gather_rates = gather_peak(mesh, local) if rank == 0 else (None, None)   # micro-benchmark, before the timed region
     for _ in range(warmup):
         step(False)
     sync_all()
@@ -578,9 +580,10 @@ def measure(key, args, ctx, headline):
     gather = None
     if peak_g:
         gather = {"gather": gather_kind, "start_face_order": face_order, "record_bytes": 3 * mesh.nf * 128, "achieved_grecords_per_s": cps_fwd / 1e9,
-                  "peak_grecords_per_s": peak_g, "frac": cps_fwd / 1e9 / peak_g,
-                  "source": "scripts/micro/gather_bench run inside this bench before the timed region: RANDOM records, so a "
-                            "launch scheduled in start-face order (L2 hits between neighbouring traces) can exceed it"}
+                  "peak_grecords_per_s": peak_g, "frac": cps_fwd / 1e9 / peak_g, "random_gather_grecords_per_s": gather_rates,
+                  "source": "scripts/micro/gather_bench run inside this bench before the timed region; peak = the best of its "
+                            "three gathers on RANDOM records of this array size (a launch scheduled in start-face order gets "
+                            "L2 hits between neighbouring traces that random records do not)"}
     bwd_ms = float(np.mean(step_ms) - np.mean(tr_ms)) if scheme != "gfd" else separate["ms_per_step"] - separate["forward_ms"]
     line = {"metric": f"face_crossings_per_s_fwd_{scheme}" if scheme != "fwd" else "face_crossings_per_s_fwd",
             "value": value, "unit": "face-crossings/s", "n_gpus": world, "steps": steps, "warmup": warmup,
