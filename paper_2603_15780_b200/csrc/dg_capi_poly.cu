@@ -155,16 +155,29 @@ static int trace_polylines_small(const dg_mesh* mesh, int64_t n, const dg_trace_
   }
   char* hp = ps.small_host;
   char* dp = ps.small_dev;
+  // The smallest batches skip every copy (as dg_trace_batch does up to 256 queries): the pinned blocks are mapped
+  // into the device's address space, the walker reads its queries from and writes its results to the host block,
+  // the scan + compaction block writes the offsets and the packed polylines straight into the host arrays; only
+  // the work counters and the slots live in device memory. One memset, two launches, one synchronisation.
+  const bool mapped = n <= 256 && slots <= (size_t(1) << 18);
+  if (mapped && ps.points_bytes < PackedPoints(slots).bytes) {
+    cudaFreeHost(ps.points); ps.points = nullptr; ps.points_bytes = 0;
+    const size_t want = std::max<size_t>(PackedPoints(slots).bytes, size_t(1) << 16);
+    DG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ps.points), want));
+    ps.points_bytes = want;
+  }
   std::memset(hp, 0, 32);
   for (auto& f : fin) if (f.bytes) std::memcpy(hp + f.off, f.src, f.bytes);
   cudaStream_t stream = mesh->stream;
-  DG_CUDA(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, stream));
+  if (mapped) DG_CUDA(cudaMemsetAsync(dp, 0, 32, stream));
+  else DG_CUDA(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, stream));
+  char* io = mapped ? hp : dp;   // where the walker finds the request and leaves the results
 
   dg::TraceParams p{};
   mesh->bind(p);
   p.n = n;
-  auto din = [&](int i) { return fin[i].bytes ? dp + fin[i].off : nullptr; };
-  auto dout = [&](int i) { return fout[i].bytes ? dp + fout[i].off : nullptr; };
+  auto din = [&](int i) { return fin[i].bytes ? io + fin[i].off : nullptr; };
+  auto dout = [&](int i) { return fout[i].bytes ? io + fout[i].off : nullptr; };
   p.face = reinterpret_cast<const int32_t*>(din(0)); p.bary = reinterpret_cast<const double*>(din(1));
   p.dir = reinterpret_cast<const double*>(din(2)); p.payload = reinterpret_cast<const double*>(din(3));
   p.o_face = reinterpret_cast<int32_t*>(dout(0)); p.o_bary = reinterpret_cast<double*>(dout(1));
@@ -187,10 +200,10 @@ static int trace_polylines_small(const dg_mesh* mesh, int64_t n, const dg_trace_
   p.want_q = c.want_transport_matrix;
   DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, true, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm), int(c.walker)}, stream));
   poly_scan_compact_small_kernel<<<1, 1024, 0, stream>>>(p.o_npoints, d_off, int(n), cap, p.poly_face, p.poly_bary, p.poly_seg,
-                                                         dp + packed_off, ctr + 2);
+                                                         mapped ? ps.points : dp + packed_off, ctr + 2);
   DG_CUDA(cudaGetLastError());
   DG_CUDA(cudaMemcpyAsync(hp, dp, 32, cudaMemcpyDeviceToHost, stream));
-  DG_CUDA(cudaMemcpyAsync(hp + out_begin, dp + out_begin, io_bytes - out_begin, cudaMemcpyDeviceToHost, stream));
+  if (!mapped) DG_CUDA(cudaMemcpyAsync(hp + out_begin, dp + out_begin, io_bytes - out_begin, cudaMemcpyDeviceToHost, stream));
   DG_CUDA(cudaStreamSynchronize(stream));
   const int64_t* h_off = reinterpret_cast<const int64_t*>(hp + fout[12].off);
   const size_t T = size_t(h_off[N]);
@@ -204,7 +217,7 @@ static int trace_polylines_small(const dg_mesh* mesh, int64_t n, const dg_trace_
     DG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ps.points), want));
     ps.points_bytes = want;
   }
-  if (T) {
+  if (T && !mapped) {
     DG_CUDA(cudaMemcpyAsync(ps.points, dp + packed_off, pk.bytes, cudaMemcpyDeviceToHost, stream));
     DG_CUDA(cudaStreamSynchronize(stream));
   }

@@ -1,13 +1,29 @@
 #!/bin/bash
-# Round-2 ncu evidence (run under gpurun; reports land in gpurun_out/, summaries are made from them into profiles/).
+# Round-2 ncu evidence (run under gpurun). Every capture is summarised ON THE BOX into gpurun_out/profiles_r2/
+# (raw metric CSV, SASS summary, per-source-line profile) and the .ncu-rep is dropped: six reports with imported
+# sources exceed what gpurun copies back.
 set -x
+OUT=gpurun_out/profiles_r2
+mkdir -p $OUT /tmp/prof
 NCU="ncu --set full --clock-control none --import-source on"
-$NCU -k regex:trace_fast_kernel -s 2 -c 1 -o gpurun_out/r2_c2_forward            python scripts/profile_target.py c2 forward exact
-$NCU -k regex:trace_fast_kernel -s 2 -c 1 -o gpurun_out/r2_c2_forward_fastlane   python scripts/profile_target.py c2 forward fast
-$NCU -k regex:trace_fast_kernel -s 2 -c 1 -o gpurun_out/r2_c3_forward            python scripts/profile_target.py c3 forward exact
-$NCU -k "regex:trace_fast_kernel<1, 0, 0, 1" -s 2 -c 1 -o gpurun_out/r2_c3_fused_gfd  python scripts/profile_target.py c3 fused exact
-$NCU -k regex:trace_fast_kernel -s 2 -c 1 -o gpurun_out/r2_c4_forward            python scripts/profile_target.py c4 forward exact
-$NCU -k regex:trace_fast_kernel -s 2 -c 1 -o gpurun_out/r2_c5_forward            python scripts/profile_target.py c5 forward exact 500000
+LIB=paper_2603_15780_b200/lib/libdigeo_b200.so
+(cd /tmp/prof && cuobjdump -xelf dg_trace_kernel.sm_100a.cubin $OLDPWD/$LIB > /dev/null && nvdisasm -g -c dg_trace_kernel.sm_100a.cubin > /tmp/prof/trace_dis.txt)
+capture() {  # name, kernel regex, mangled-name substring for the line profile, command...
+  local name=$1 regex=$2 mangled=$3; shift 3
+  $NCU -k "$regex" -s 2 -c 1 -f -o /tmp/prof/$name "$@" > $OUT/$name.log 2>&1
+  ncu -i /tmp/prof/$name.ncu-rep --page raw --csv > $OUT/${name}_raw.csv 2>/dev/null
+  ncu -i /tmp/prof/$name.ncu-rep --page source --csv --print-source sass > /tmp/prof/${name}_sass.csv 2>/dev/null
+  python profiles/ncu_sass_summary.py /tmp/prof/${name}_sass.csv > $OUT/${name}_sass_summary.txt 2>&1
+  python profiles/ncu_line_profile.py /tmp/prof/${name}_sass.csv /tmp/prof/trace_dis.txt "$mangled" > $OUT/${name}_line_profile.txt 2>&1
+  rm -f /tmp/prof/$name.ncu-rep /tmp/prof/${name}_sass.csv
+}
+capture r2_c2_forward          regex:trace_fast_kernel "trace_fast_kernelILb1ELi0ELi0ELb0ELi0" python scripts/profile_target.py c2 forward exact
+capture r2_c2_forward_fastlane regex:trace_fast_kernel "trace_fast_kernelILb1ELi0ELi0ELb0ELi1" python scripts/profile_target.py c2 forward fast
+capture r2_c3_forward          regex:trace_fast_kernel "trace_fast_kernelILb1ELi0ELi0ELb0ELi0" python scripts/profile_target.py c3 forward exact
+capture r2_c3_fused_gfd        "regex:trace_fast_kernel<1, 0, 0, 1" "trace_fast_kernelILb1ELi0ELi0ELb1ELi0" python scripts/profile_target.py c3 fused exact
+capture r2_c4_forward          regex:trace_fast_kernel "trace_fast_kernelILb1ELi0ELi0ELb0ELi0" python scripts/profile_target.py c4 forward exact
+capture r2_c5_forward          regex:trace_fast_kernel "trace_fast_kernelILb1ELi0ELi0ELb0ELi0" python scripts/profile_target.py c5 forward exact 500000
 # every launch of a short default bench run with its device time (cold-cache, serialised: compare SHARES)
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2_launches_bench.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/r2_launches_bench.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/r2_launches_bench.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/r2_launches_bench.log 2>&1
+ls -la $OUT

@@ -1,0 +1,36 @@
+"""the reference's `digeo benchmark` protocol (digeo_main.cpp:232-286: batch sweep on icosphere-4,
+face sweep at batch 2 000, 5 repetitions, median) with a gpu back-end column, the reference's DEFAULT
+record_polyline = true on every back-end. Pins what the one-call polyline path is for: from batch 1 000 up the GPU
+call (host buffers, copies included) beats the reference's parallel back-end on the box's host cores, and at
+batch 100 -- 3 000 face crossings, a tenth of a millisecond of CPU work -- it stays within 2.5 x of it."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_benchmark_protocol_with_gpu_backend(gpu, ref):
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    import benchmark_sweep
+    best = {}
+    for attempt in range(3):     # medians of 5 on a shared host: keep the best of three sweeps per cell
+        rows = benchmark_sweep.sweep(batches=(100, 1000, 10000), subdivs=(3, 5), reps=5,
+                                     backends=("parallel", "gpu", "gpu_nopolyline"))
+        for section, mesh, faces, batch, backend, med, *_ in rows:
+            key = (section, mesh, batch, backend)
+            best[key] = min(best.get(key, np.inf), med)
+    cell = lambda section, mesh, batch, backend: best[(section, mesh, batch, backend)]
+    for batch in (1000, 10000):
+        assert cell("batch_sweep", "icosphere4", batch, "gpu") < cell("batch_sweep", "icosphere4", batch, "parallel"), batch
+    assert cell("batch_sweep", "icosphere4", 100, "gpu") < 2.5 * cell("batch_sweep", "icosphere4", 100, "parallel")
+    for mesh in ("icosphere3", "icosphere5"):
+        assert cell("face_sweep", mesh, 2000, "gpu") < cell("face_sweep", mesh, 2000, "parallel"), mesh
+    # polylines cost at most ~4 x the plain call at 10 000 traces (30 points of 36 bytes per trace come back)
+    assert cell("batch_sweep", "icosphere4", 10000, "gpu") < 4.0 * cell("batch_sweep", "icosphere4", 10000, "gpu_nopolyline")
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        benchmark_sweep.write_csv(rows, os.path.join(out, "benchmark_sweep_test.csv"))
