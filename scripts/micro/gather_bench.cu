@@ -29,6 +29,24 @@ __global__ void __launch_bounds__(128, 4) gather_ldg(const char* rec, uint32_t n
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// (d) 64-byte records, two 256-bit loads per lane: what a half-size crossing record would cost to gather
+// (prototype measurement for a tolerance-lane layout; the next index sits in the low word of the 8th double)
+__global__ void __launch_bounds__(128, 4) gather_ldg64(const char* rec, uint32_t nrec, int iters, double* out) {
+  uint32_t idx = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u % nrec;
+  double acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    const char* p = rec + size_t(idx) * 64;
+    double v[8];
+    ldg256(p, v[0], v[1], v[2], v[3]); ldg256(p + 32, v[4], v[5], v[6], v[7]);
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) s += v[k];
+    acc += s;
+    idx = uint32_t(__double2loint(v[7])) % nrec;
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 constexpr int kStride = 144;  // bytes per lane slot in shared memory (128 + 16: conflict-free 128-bit reads)
 
 __global__ void __launch_bounds__(128, 4) gather_tma(const char* rec, uint32_t nrec, int iters, double* out) {
@@ -126,6 +144,28 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaFuncSetAttribute(gather_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const int only = argc > 3 ? atoi(argv[3]) : -1;   // one variant, machine-readable: bench.py's gather ceiling
+  if (only == 3) {   // 64-byte records: the same array read as 2 nrec half-size records
+    const uint32_t n64 = nrec;   // (argv[1] counts 64-byte records in this mode; the array holds nrec * 64 bytes of them)
+    double* h64 = (double*)malloc(size_t(n64) * 64);
+    uint32_t y = 12345;
+    for (uint32_t r = 0; r < n64; ++r) {
+      for (int k = 0; k < 7; ++k) h64[size_t(r) * 8 + k] = 1e-3 * k;
+      y = y * 1664525u + 1013904223u;
+      uint64_t bits = y % n64;
+      memcpy(&h64[size_t(r) * 8 + 7], &bits, 8);
+    }
+    cudaMemcpy(rec, h64, size_t(n64) * 64, cudaMemcpyHostToDevice);
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(e0);
+      gather_ldg64<<<blocks, threads>>>(rec, n64, iters, out);
+      cudaEventRecord(e1);
+      cudaError_t err = cudaDeviceSynchronize();
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      if (rep == 2) printf("{\"variant\": 3, \"records\": %u, \"record_bytes\": 64, \"ms\": %.4f, \"grecords_per_s\": %.4f, \"cuda\": \"%s\"}\n",
+                           n64, ms, double(blocks) * threads * iters / ms / 1e6, cudaGetErrorString(err));
+    }
+    return 0;
+  }
   for (int variant = 0; variant < 3; ++variant) {
     if (only >= 0 && variant != only) continue;
     for (int rep = 0; rep < 3; ++rep) {

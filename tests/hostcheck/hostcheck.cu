@@ -33,7 +33,7 @@ struct HostMesh {
 
 // The fast walker (csrc/dg_fast_walk.cuh) driven the way trace_fast_kernel drives a lane: lean
 // start-up, fast steps, the generic paths for everything the fast step hands back.
-template <bool kCached, int kPay>
+template <bool kCached, int kPay, int kLane = 0>
 void run_fast(const HostMesh& hm, const TraceParams& p) {
 #pragma omp parallel for schedule(dynamic, 8)
   for (int64_t q = 0; q < p.n; ++q) {
@@ -46,7 +46,7 @@ void run_fast(const HostMesh& hm, const TraceParams& p) {
     }
     while (live) {
       StepSpill sp;
-      const int action = fast_step<kCached, false, kPay>(p, L, sp);
+      const int action = fast_step<kCached, false, kPay, kLane>(p, L, sp);
       if (action == kActFast) continue;
       if (action == kActFinish) {
         fast_finish<kCached, kPay>(p, q, L, sp);
@@ -102,6 +102,8 @@ void run_batch(const HostMesh& hm, int64_t n, const int32_t* face, const double*
 }
 
 }  // namespace
+
+static int g_lane_fast = 0;
 
 HC_API void* hc_mesh_create(const double* xyz, int32_t nv, const int32_t* tri, int32_t nf, const int32_t* adj,
                             const double* fnormal, const double* vangle, const uint8_t* vboundary,
@@ -169,5 +171,9 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
   p.want_q = uint8_t(want_q != 0); p.o_transport = o_q;
   if (want_q) { if (cached) run_fast<true, 2>(hm, p); else run_fast<false, 2>(hm, p); }
   else if (payload || hole || poly_off) { if (cached) run_fast<true, 1>(hm, p); else run_fast<false, 1>(hm, p); }
+  else if (cached && g_lane_fast) run_fast<true, 0, 1>(hm, p);   // DG_LANE_FAST: the tolerance lane of the fast step
   else { if (cached) run_fast<true, 0>(hm, p); else run_fast<false, 0>(hm, p); }
 }
+
+// 1: plain forward requests over crossing records run the tolerance lane (dg_trace_cfg.lane = DG_LANE_FAST)
+HC_API void hc_set_lane_fast(int on) { g_lane_fast = on; }

@@ -88,7 +88,7 @@ class HostMesh:
         return r
 
     def trace_batch_fast(self, face, bary, dirs, max_steps=0, cached=False, payload=None, hole_avoidance=False,
-                         record_polyline=False, want_q=False):
+                         record_polyline=False, want_q=False, lane_fast=False):
         """The fast walker (csrc/dg_fast_walk.cuh: fast_init / fast_step / fast_finish + the generic
         paths behind them) driven on the host the way trace_fast_kernel drives a lane."""
         face, bary, dirs, payload = _i32(face), _f64(bary), _f64(dirs), _f64(payload)
@@ -105,12 +105,16 @@ class HostMesh:
         if want_q:
             r.q = np.empty((n, 9))
 
+        lib().hc_set_lane_fast(int(lane_fast))
+
         def call(off, pf, pb, ps):
             lib().hc_trace_batch_fast(self.h, C.c_int64(n), _p(face), _p(bary), _p(dirs), _p(payload), _p(r.payload),
                                       int(hole_avoidance), int(want_q), _p(r.q), int(max_steps), int(cached), _p(r.face), _p(r.bary), _p(r.dir),
                                       _p(r.traced), _p(r.requested), _p(r.term), _p(r.status), _p(r.stall), _p(r.npoints),
                                       _p(r.crossings), _p(off), _p(pf), _p(pb), _p(ps))
         call(None, None, None, None)
+        if lane_fast:
+            lib().hc_set_lane_fast(0)
         if record_polyline:   # the two passes of the C-ABI: count, scan, fill
             off = np.zeros(n + 1, np.int64)
             np.cumsum(r.npoints, out=off[1:])

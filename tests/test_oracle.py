@@ -186,3 +186,31 @@ def test_oracle_vs_reference_fresh_inputs(oracle, ref):
                       "poly_bary", "poly_seg"):
                 assert _equal(np.asarray(getattr(r, k), float), np.asarray(getattr(o, k), float)), (k, hole)
             assert r.errors == o.errors
+
+
+def test_tolerance_lane_on_host_vs_reference(hostcheck, ref):
+    """DG_LANE_FAST (the opt-in tolerance lane of the fast step: reciprocal-multiply quotients, one reciprocal for the
+    exit parameter, no second renormalising snap, first-order direction renormalisation), compiled for the host and
+    driven the way the kernel drives a lane, against the unmodified reference: identical end faces, termination and
+    point counts -- i.e. the same walks, every way out of the fast step included --, end points within 1e-9 x bbox
+    diagonal, directions within 1e-9, lengths within 1e-9 relative; and it really is another arithmetic (not
+    bit-equal on plain traces)."""
+    cases = [(ref.RefMesh.icosphere(4), 91, 0.1, 3.0), (ref.RefMesh.torus(1 / 3, 1 / 6, 48, 24), 92, 0.05, 2.0),
+             (ref.RefMesh.plane(10, 8, 1.0, 0), 93, 0.05, 2.0)]
+    for rm, seed, lo, hi in cases:
+        hm = hostcheck.HostMesh(rm.arrays())
+        f, b, d = rm.sample_queries(seed, 4000, lo, hi)
+        b[400:500] = [0.5, 0.5, 0.0]        # edge starts
+        b[500:600] = [0.0, 1.0, 0.0]        # vertex starts
+        f[600] = -1; d[602] = 0.0
+        theirs = rm.trace_batch(f, b, d, record_polyline=True)
+        ours = hm.trace_batch_fast(f, b, d, max_steps=rm.default_max_steps(), cached=True, lane_fast=True)
+        for k in ("face", "term", "status", "npoints"):
+            assert np.array_equal(getattr(theirs, k), getattr(ours, k)), k
+        diag = np.linalg.norm(rm.xyz.max(0) - rm.xyz.min(0))
+        ok = theirs.face >= 0
+        assert np.abs(rm.embed(ours.face[ok], ours.bary[ok]) - rm.embed(theirs.face[ok], theirs.bary[ok])).max() <= 1e-9 * diag
+        assert np.abs(ours.dir - theirs.dir).max() <= 1e-9
+        assert np.abs(ours.traced - theirs.traced).max() <= 1e-9 * max(1.0, np.abs(theirs.traced).max())
+        plain = ok & (theirs.npoints > 3)
+        assert not np.array_equal(ours.bary[plain], theirs.bary[plain])
