@@ -80,12 +80,15 @@ enum { DG_WALKER_AUTO = 0, DG_WALKER_GENERIC = 1, DG_WALKER_FAST_LOADS = 2, DG_W
  * the parity anchor) follows the reference's operation order, so a trace that never takes a vertex branch (no libm
  * calls) is bit-identical to the reference CPU build; vertex branches agree to the last ulp of atan2/sin/cos.
  * DG_LANE_FAST is an opt-in TOLERANCE lane of the plain forward map (f64, crossing records, no payload / transport
- * matrix / polylines / hole avoidance; other requests run the exact lane): same decisions and tolerances, but
- * reciprocal-multiply instead of correctly rounded quotients, one reciprocal for the exit parameter, no second
- * renormalising snap, first-order renormalisation of the transported direction. Its bar is north_star's: identical
- * face sequences on non-degenerate queries, end points / directions within 1e-9 x bbox diagonal (measured: <= 1e-13),
- * GFD Jacobians within 1e-5 relative -- not bit equality. With dg_diff_cfg.lane it applies to GFD's full-length
- * re-traces (and the fused forward). */
+ * matrix / polylines / hole avoidance; other requests run the exact lane): same decisions and tolerances as the exact
+ * lane, cheaper arithmetic. It walks over HALF-SIZE crossing records (64 bytes: shared edge vector, third vertex of the
+ * entered face, 1 / |edge|; built on the first request of the lane, + 192 B per face) with the fold in intrinsic form --
+ * the unit direction lies in the plane of the face it leaves, so its transported image is e (d.e) + in_to sqrt(1 -
+ * (d.e)^2) and the barycentric velocity in the entered face follows from the same numbers: no in_from, no Gram solve,
+ * rsqrt instead of sqrt + divisions -- with reciprocal-multiply quotients, one reciprocal for the exit parameter and a
+ * first-order renormalisation of the direction. Its bar is north_star's: identical face sequences on non-degenerate
+ * queries, end points / directions within 1e-9 x bbox diagonal (measured: <= 1e-13), GFD Jacobians within 1e-5
+ * relative -- not bit equality. With dg_diff_cfg.lane it applies to GFD's full-length re-traces (and the fused forward). */
 enum { DG_LANE_DEFAULT = 0, DG_LANE_EXACT = 1, DG_LANE_FAST = 2 };
 
 DG_API const char* dg_last_error(void);

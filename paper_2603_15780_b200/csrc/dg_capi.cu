@@ -79,6 +79,12 @@ __global__ void build_halfedges_kernel(const dg::MeshView m, dg::HalfEdgeRec* he
   he[s] = r;
 }
 
+__global__ void build_halfedges64_kernel(const dg::MeshView m, dg::HalfEdgeRec64* he) {
+  const int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (s >= 3 * int64_t(m.nf)) return;
+  he[s] = dg::make_halfedge_rec64(m, int(s / 3), int(s % 3));
+}
+
 // Tensor map of the crossing records for the TMA tile::gather4 fetch of the fast walker: a 2-D
 // f64 tensor [3 nf rows][16 doubles], box = one row, 128-byte swizzle. The driver entry point is
 // taken through the runtime so that the library does not link libcuda.
@@ -128,6 +134,21 @@ __global__ void sort_keys_kernel(const int32_t* __restrict__ face, const double*
 static bool schedules_by_face(const dg_mesh* mesh, int64_t n, const dg_trace_cfg& c, bool record) {
   const bool big_mesh = mesh->he && size_t(3) * size_t(mesh->nf) * sizeof(dg::HalfEdgeRec) > (size_t(96) << 20);
   return c.sort_by_face == DG_SORT_ON || (c.sort_by_face == DG_SORT_AUTO && big_mesh && n >= (int64_t(1) << 15) && !record);
+}
+
+void dgapi::ensure_he64(const dg_mesh* m) {
+  if (!m || !m->he) return;
+  std::lock_guard<std::mutex> lock(m->he64_mu);
+  if (m->he64_tried) return;
+  m->he64_tried = true;
+  const size_t bytes = size_t(3) * size_t(m->nf) * sizeof(dg::HalfEdgeRec64);
+  if (bytes > (size_t(8) << 30)) return;
+  DeviceGuard guard(m->device);
+  dg::HalfEdgeRec64* p = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&p), bytes) != cudaSuccess) { cudaGetLastError(); return; }
+  build_halfedges64_kernel<<<unsigned((size_t(3) * size_t(m->nf) + 127) / 128), 128, 0, m->stream>>>(m->view_uncached(), p);
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(m->stream) != cudaSuccess) { cudaGetLastError(); cudaFree(p); return; }
+  m->he64 = p;
 }
 
 namespace dg {
@@ -436,6 +457,7 @@ void dg_mesh_destroy(dg_mesh* m) {
   poly_store_free(m->poly);
   if (m->small_pin) cudaFreeHost(m->small_pin);
   cudaFree(m->small_dev);
+  cudaFree(m->he64);
   cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
   cudaFree(m->csr_list); cudaFree(m->vboundary);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -571,6 +593,7 @@ static int trace_small(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, co
     DG_CUDA(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, stream));
   }
 
+  if (c.lane == DG_LANE_FAST) ensure_he64(mesh);
   dg::TraceParams p{};
   mesh->bind(p);
   p.n = n;
@@ -627,6 +650,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   const bool device_mode = c.memory == DG_MEM_DEVICE;
   const size_t N = size_t(n);
   auto at = [](auto* ptr, size_t) { return ptr; };
+  if (c.lane == DG_LANE_FAST) ensure_he64(mesh);
   dg::TraceParams p{};
   mesh->bind(p);
   p.n = n;

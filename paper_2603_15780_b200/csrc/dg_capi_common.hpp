@@ -54,8 +54,14 @@ struct dg_mesh {
   // at the request index. A replica has no replicas of its own.
   std::vector<dg_mesh*> replicas;
 
+  // the tolerance lane's half-size crossing records (dg_mesh_view.cuh), built by the first DG_LANE_FAST request
+  mutable dg::HalfEdgeRec64* he64 = nullptr;
+  mutable std::mutex he64_mu;
+  mutable bool he64_tried = false;
   dg::MeshView view() const {
-    return dg::MeshView{rec, he, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
+    dg::MeshView v{rec, he, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
+    v.he64 = he64;
+    return v;
   }
   // the same mesh without the transport cache (f32 lane: its transports are float arithmetic)
   dg::MeshView view_uncached() const {
@@ -250,6 +256,9 @@ class PeerStage {
 };
 
 void poly_store_free(dg_poly_store* s);
+// Builds the half-size records of the tolerance lane on first use (no-op afterwards; quietly leaves he64 null when
+// the mesh has no crossing records or the memory is not there: the lane then runs over the 128-byte records).
+void ensure_he64(const dg_mesh* mesh);
 // one-device forms of the resident batch (the dg_batch_* entry points dispatch over the devices of a multi-GPU mesh)
 int trace_batch_one(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c, dg_trace_out* out);
 int batch_create_one(const dg_mesh* mesh, int64_t capacity, dg_batch** out);

@@ -406,6 +406,7 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   // tolerance lane -- all of them, so that the differences are taken between like and like. With a known base the
   // caller's forward traces must come from the same lane.
   const bool lane_fast = c.lane == DG_LANE_FAST;
+  if (lane_fast) ensure_he64(mesh);
 
   Stage st(stream, device_mode);
   const size_t N = size_t(n);

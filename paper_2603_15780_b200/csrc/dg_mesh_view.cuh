@@ -45,6 +45,23 @@ struct alignas(128) HalfEdgeRec {
 };
 static_assert(sizeof(HalfEdgeRec) == 128, "HalfEdgeRec must be one 128-byte line");
 
+// The crossing record of the TOLERANCE lane (DG_LANE_FAST): half the size. In the intrinsic form of the fold a
+// crossing needs the shared edge vector E = xc - xa, the third vertex of the entered face relative to xa, W = xt - xa,
+// and 1 / |E|: with e = E / |E| and in_to = unit(W - e (W.e)) the transported direction is
+// e (d.e) + in_to sqrt(1 - (d.e)^2) -- the unit direction d lies in the plane of the face it leaves, so its component
+// along that face's inward edge normal is -sqrt(1 - (d.e)^2) and in_from is never needed --, and the barycentric
+// velocity in the entered face follows from the same numbers (v_t = beta / |W_perp|, v_c = (alpha - v_t W.e) / |E|)
+// without a Gram solve. Not the reference's operation sequence: results agree to rounding (1e-13 of the diagonal),
+// not to the bit, which is why only the tolerance lane reads it. One 64-byte half line = two 32-byte sectors.
+struct alignas(64) HalfEdgeRec64 {
+  double E[3];      // xc - xa (a, c: the end points of the crossed edge, corners (k + 1) % 3 and (k + 2) % 3 of the face left)
+  double W[3];      // xt - xa (t: the third vertex of the entered face)
+  double inv_len;   // 1 / |E|
+  int32_t g;        // face entered (-1 = boundary)
+  int32_t corners;  // ja | jc << 2 | jt << 4, as HalfEdgeRec
+};
+static_assert(sizeof(HalfEdgeRec64) == 64, "HalfEdgeRec64 must be two 32-byte sectors");
+
 struct MeshView {
   const FaceRec* rec;        // [nf]
   const HalfEdgeRec* he;     // [3 nf] or null (transport cache off)
@@ -54,6 +71,7 @@ struct MeshView {
   const int32_t* csr_list;   // [3 nf]
   const uint8_t* vboundary;  // [nv]   (Mesh::vertex_on_boundary)
   int32_t nf, nv;
+  const HalfEdgeRec64* he64 = nullptr;  // [3 nf] or null: the tolerance lane's half-size crossing records
 };
 
 // Register copy of one face record in the stepping scalar type S.

@@ -244,7 +244,12 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
                        : launch_fast<true, 0, kPay>(p, shape, stream);
   };
   if (!needs_full && shape.walker != 1 && fast_walk_enabled()) {
-    if (p.lane_fast && p.mesh.he) {   // DG_LANE_FAST: the tolerance lane of the plain forward map (dg_fast_walk.cuh)
+    if (p.lane_fast && p.mesh.he64 && !std::getenv("DG_LANE_FAST_128")) {
+      // DG_LANE_FAST: the tolerance lane over half-size records, intrinsic fold (HalfEdgeRec64)
+      if (p.siblings > 1) return launch_fast<true, 0, 0, true, 2>(p, shape, stream);
+      return launch_fast<true, 0, 0, false, 2>(p, shape, stream);
+    }
+    if (p.lane_fast && p.mesh.he) {   // ... over the 128-byte records (no half-size records on this mesh)
       if (gather == 0 && p.siblings > 1) return launch_fast<true, 0, 0, true, 1>(p, shape, stream);
       return gather == 0 ? launch_fast<true, 0, 0, false, 1>(p, shape, stream) : launch_fast<true, 2, 0, false, 1>(p, shape, stream);
     }

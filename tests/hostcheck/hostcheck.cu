@@ -21,13 +21,16 @@ namespace {
 struct HostMesh {
   std::vector<FaceRec> rec;
   std::vector<HalfEdgeRec> he;  // crossing records (built on demand by the same function the upload kernel runs)
+  std::vector<HalfEdgeRec64> he64;  // the tolerance lane's half-size records (ditto)
   std::vector<double> fnormal, vangle;
   std::vector<int32_t> csr_off, csr_list;
   std::vector<uint8_t> vboundary;
   int32_t nf, nv;
   MeshView view(bool cached = false) const {
-    return MeshView{rec.data(), cached ? he.data() : nullptr, fnormal.data(), vangle.data(), csr_off.data(),
-                    csr_list.data(), vboundary.data(), nf, nv};
+    MeshView v{rec.data(), cached ? he.data() : nullptr, fnormal.data(), vangle.data(), csr_off.data(),
+               csr_list.data(), vboundary.data(), nf, nv};
+    v.he64 = cached && !he64.empty() ? he64.data() : nullptr;
+    return v;
   }
 };
 
@@ -157,6 +160,12 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
     for (int f = 0; f < hm.nf; ++f)
       for (int k = 0; k < 3; ++k) hm.he[3 * size_t(f) + k] = make_halfedge_rec(mv, f, k);
   }
+  if (cached && g_lane_fast == 2 && hm.he64.empty()) {
+    hm.he64.resize(3 * size_t(hm.nf));
+    const MeshView mv = hm.view(false);
+    for (int f = 0; f < hm.nf; ++f)
+      for (int k = 0; k < 3; ++k) hm.he64[3 * size_t(f) + k] = make_halfedge_rec64(mv, f, k);
+  }
   TraceParams p{};
   p.snap_hi = 1.0 - 1e-10;
   p.mesh = hm.view(cached != 0);
@@ -171,9 +180,11 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
   p.want_q = uint8_t(want_q != 0); p.o_transport = o_q;
   if (want_q) { if (cached) run_fast<true, 2>(hm, p); else run_fast<false, 2>(hm, p); }
   else if (payload || hole || poly_off) { if (cached) run_fast<true, 1>(hm, p); else run_fast<false, 1>(hm, p); }
-  else if (cached && g_lane_fast) run_fast<true, 0, 1>(hm, p);   // DG_LANE_FAST: the tolerance lane of the fast step
+  else if (cached && g_lane_fast == 2) run_fast<true, 0, 2>(hm, p);   // DG_LANE_FAST over half-size records (intrinsic fold)
+  else if (cached && g_lane_fast) run_fast<true, 0, 1>(hm, p);        // DG_LANE_FAST over the 128-byte records
   else { if (cached) run_fast<true, 0>(hm, p); else run_fast<false, 0>(hm, p); }
 }
 
-// 1: plain forward requests over crossing records run the tolerance lane (dg_trace_cfg.lane = DG_LANE_FAST)
+// 1 / 2: plain forward requests over crossing records run the tolerance lane (dg_trace_cfg.lane = DG_LANE_FAST) over
+// the 128-byte records / over the half-size records
 HC_API void hc_set_lane_fast(int on) { g_lane_fast = on; }

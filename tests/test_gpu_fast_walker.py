@@ -241,10 +241,13 @@ def test_randomised_meshes_scales_and_starts(gpu):
     assert fuzz_walkers.main(rounds=24, n=6000, seed=11) == 0
 
 
+@pytest.mark.parametrize("records", ["half-size", "128-byte"])
 @pytest.mark.parametrize("key,n", [("c1", 10_000), ("c2", 200_000), ("c3", 60_000)])
-def test_tolerance_lane_parity_gate(gpu, ref, key, n):
-    """DG_LANE_FAST, the opt-in tolerance lane of the plain forward map (reciprocal-multiply quotients, one reciprocal
-    for the exit parameter, no second renormalising snap, first-order renormalisation of the direction). Its bar is
+def test_tolerance_lane_parity_gate(gpu, ref, key, n, records, monkeypatch):
+    """DG_LANE_FAST, the opt-in tolerance lane of the plain forward map: the intrinsic fold over half-size (64-byte)
+    crossing records -- no in_from, no Gram solve, rsqrt normalisation -- and, where a mesh has no such records
+    (DG_LANE_FAST_128 forces it here), the fast step over the 128-byte records with reciprocal-multiply quotients, one
+    reciprocal for the exit parameter, no second renormalising snap, first-order renormalisation. Its bar is
     north_star's, stated here: identical face sequences and end faces on the (non-degenerate) random queries of
     configs 1-3, end points within 1e-9 x bbox diagonal, directions within 1e-9, traced length within 1e-9 relative --
     against the EXACT lane and against the UNMODIFIED reference; GFD Jacobians through the lane within 1e-5 relative
@@ -257,6 +260,8 @@ def test_tolerance_lane_parity_gate(gpu, ref, key, n):
         f, b, d = W.sample_queries(xyz, tri, n, 1.0, seed=42)
     else:
         xyz, tri, f, b, d, _ = make_workload(key, n, 42)
+    if records == "128-byte":
+        monkeypatch.setenv("DG_LANE_FAST_128", "1")
     m = gpu.Mesh(xyz, tri)
     diag = W.bbox_diagonal(xyz)
     exact = m.trace_batch(f, b, d, sort_by_face=False)

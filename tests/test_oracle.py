@@ -188,7 +188,8 @@ def test_oracle_vs_reference_fresh_inputs(oracle, ref):
             assert r.errors == o.errors
 
 
-def test_tolerance_lane_on_host_vs_reference(hostcheck, ref):
+@pytest.mark.parametrize("records", [1, 2], ids=["128-byte records", "half-size records"])
+def test_tolerance_lane_on_host_vs_reference(hostcheck, ref, records):
     """DG_LANE_FAST (the opt-in tolerance lane of the fast step: reciprocal-multiply quotients, one reciprocal for the
     exit parameter, no second renormalising snap, first-order direction renormalisation), compiled for the host and
     driven the way the kernel drives a lane, against the unmodified reference: identical end faces, termination and
@@ -204,7 +205,7 @@ def test_tolerance_lane_on_host_vs_reference(hostcheck, ref):
         b[500:600] = [0.0, 1.0, 0.0]        # vertex starts
         f[600] = -1; d[602] = 0.0
         theirs = rm.trace_batch(f, b, d, record_polyline=True)
-        ours = hm.trace_batch_fast(f, b, d, max_steps=rm.default_max_steps(), cached=True, lane_fast=True)
+        ours = hm.trace_batch_fast(f, b, d, max_steps=rm.default_max_steps(), cached=True, lane_fast=records)
         for k in ("face", "term", "status", "npoints"):
             assert np.array_equal(getattr(theirs, k), getattr(ours, k)), k
         diag = np.linalg.norm(rm.xyz.max(0) - rm.xyz.min(0))
