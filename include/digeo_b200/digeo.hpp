@@ -309,9 +309,11 @@ class ResidentBatch {
   ~ResidentBatch();
   ResidentBatch(const ResidentBatch&) = delete;
   ResidentBatch& operator=(const ResidentBatch&) = delete;
-  // plain forward exp map (cfg: max_steps / use_f32 only)
+  // plain forward exp map (cfg: max_steps / use_f32 only). gfd_follows != nullptr: the backward of this step will be
+  // gfd(*gfd_follows, g) -- forward and Jacobians are then computed in one pass (the forward traces are GFD's base
+  // traces, diff.cpp:288-294) and gfd() only pulls g back; same results as the separate calls.
   TraceSoA trace(std::span<const int32_t> face, std::span<const double> bary, std::span<const double> dir,
-                 const TraceConfig& cfg = {});
+                 const TraceConfig& cfg = {}, const GfdConfig* gfd_follows = nullptr);
   // grad_v [3n] of pullback_ambient(g_i, ep_jacobians(sample_i)); grad_p is identically zero
   std::vector<double> ep_backward(std::span<const double> g);
   struct Gfd {

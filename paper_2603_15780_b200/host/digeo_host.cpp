@@ -441,7 +441,7 @@ ResidentBatch::~ResidentBatch() { dg_batch_destroy(h_); }
 size_t ResidentBatch::size() const { return size_t(dg_batch_size(h_)); }
 
 TraceSoA ResidentBatch::trace(std::span<const int32_t> face, std::span<const double> bary, std::span<const double> dir,
-                              const TraceConfig& cfg) {
+                              const TraceConfig& cfg, const GfdConfig* gfd_follows) {
   const size_t n = face.size();
   if (bary.size() != 3 * n || dir.size() != 3 * n) throw InvalidArgs("trace_batch: starts and dirs differ in length");
   TraceSoA r;
@@ -453,7 +453,10 @@ TraceSoA ResidentBatch::trace(std::span<const int32_t> face, std::span<const dou
   o.face = r.face.data(); o.bary = r.bary.data(); o.dir = r.dir.data(); o.traced = r.traced.data();
   o.requested = r.requested.data(); o.term = r.term.data(); o.status = r.status.data(); o.stall = r.stall.data();
   o.crossings = r.crossings.data(); o.total_crossings = &r.total_crossings;
-  check(dg_batch_trace(h_, int64_t(n), &in, &k, &o));
+  // gfd_follows: the backward of this step will be GFD -- the forward traces ride in GFD's round 2 as the fourth
+  // sibling of their sample's re-traces, the Jacobians stay on the GPU and gfd() only pulls g back (dg_batch_trace_gfd)
+  if (gfd_follows) check(dg_batch_trace_gfd(h_, int64_t(n), &in, &k, gfd_follows->eps_v, gfd_follows->eps_p, &o));
+  else check(dg_batch_trace(h_, int64_t(n), &in, &k, &o));
   return r;
 }
 

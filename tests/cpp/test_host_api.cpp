@@ -289,6 +289,18 @@ static void test_differentials() {
       CHECK(near(Vec3d(rg.grad_v[3 * i], rg.grad_v[3 * i + 1], rg.grad_v[3 * i + 2]), pf.grad_v, 1e-12));
     }
     CHECK(throws<InvalidArgs>([&] { rb.ep_backward(std::vector<double>(3)); }));
+    // the forward of a GFD step: forward + Jacobians in one pass, the backward is the pull-back -- same bits
+    const GfdConfig gc = default_gfd_config(ico);
+    TraceSoA fused = rb.trace(face, bary, dir, {}, &gc);
+    ResidentBatch::Gfd pulled = rb.gfd(gc, gs);
+    int diff = 0;
+    for (size_t i = 0; i < n; ++i) {
+      diff += fused.face[i] != fwd.face[i] || fused.bary[3 * i] != fwd.bary[3 * i] || fused.dir[3 * i + 2] != fwd.dir[3 * i + 2] ||
+              fused.traced[i] != fwd.traced[i] || fused.crossings[i] != fwd.crossings[i];
+      diff += pulled.jv[4 * i + 1] != rg.jv[4 * i + 1] || pulled.jp[4 * i + 2] != rg.jp[4 * i + 2] ||
+              pulled.grad_v[3 * i] != rg.grad_v[3 * i] || pulled.grad_p[3 * i + 1] != rg.grad_p[3 * i + 1];
+    }
+    CHECK(diff == 0 && fused.total_crossings == fwd.total_crossings);
   }
   CHECK(throws<DegenerateDirection>([&] { ep_jacobians(ico, samples[0].p, {0, 0, 0}, traces[0]); }));
   CHECK(throws<DegenerateDirection>([&] { make_tangent_frame(ico, samples[0].p, ico.face_normals[samples[0].p.face]); }));
