@@ -88,7 +88,7 @@ enum { DG_WALKER_AUTO = 0, DG_WALKER_GENERIC = 1, DG_WALKER_FAST_LOADS = 2, DG_W
  * rsqrt instead of sqrt + divisions -- with reciprocal-multiply quotients, one reciprocal for the exit parameter and a
  * first-order renormalisation of the direction. Its bar is north_star's: identical face sequences on non-degenerate
  * queries, end points / directions within 1e-9 x bbox diagonal (measured: <= 1e-13), GFD Jacobians within 1e-5
- * relative -- not bit equality. With dg_diff_cfg.lane it applies to GFD's full-length re-traces (and the fused forward). */
+ * relative -- not bit equality (c2 forward 3.61 -> 2.67 ms, c3 15.8 -> 11.2 ms per 1 M). With dg_diff_cfg.lane it applies to GFD's full-length re-traces (and the fused forward). */
 enum { DG_LANE_DEFAULT = 0, DG_LANE_EXACT = 1, DG_LANE_FAST = 2 };
 
 DG_API const char* dg_last_error(void);
