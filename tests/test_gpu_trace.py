@@ -342,3 +342,34 @@ def test_one_call_polylines_give_the_bits_of_the_two_call_form(gpu, ref):
         assert np.array_equal(getattr(a, k), getattr(t, k)), k
     assert_trace_equal(r, a, len(f), payload=True, q=True)
     del os.environ["DG_POLY_SLOT_BUDGET"]
+
+
+def test_new_entry_points_on_empty_and_odd_requests(gpu, ref):
+    """n = 0 and n = 1 through the one-call polylines, the fused forward + GFD and the pull-back; the tolerance lane
+    asked for where it does not apply (payload, a mesh without crossing records, f32) runs the exact lane."""
+    rm = ref.RefMesh.icosphere(2)
+    a = rm.arrays()
+    m = gpu.Mesh(a["xyz"], a["tri"])
+    f, b, d = rm.sample_queries(1, 300, 0.2, 1.0)
+    z = lambda *shape: np.empty(shape)
+    e = m.trace_batch(f[:0], b[:0], d[:0], record_polyline=True)
+    assert len(e.face) == 0 and e.poly_offsets.tolist() == [0] and len(e.poly_face) == 0 and e.total_crossings == 0
+    r, jac = m.trace_gfd(f[:0], b[:0], d[:0])
+    assert len(r.face) == 0 and jac["jv"].shape == (0, 4)
+    assert m.gfd_pullback(f[:0], d[:0], f[:0], z(0, 4), z(0, 4), z(0, 3))["grad_v"].shape == (0, 3)
+    one, jac1 = m.trace_gfd(f[:1], b[:1], d[:1])
+    sep = m.gfd(f[:1], b[:1], d[:1])
+    assert np.array_equal(jac1["jv"], sep["jv"]) and np.array_equal(one.bary, m.trace_batch(f[:1], b[:1], d[:1]).bary)
+    # the lane is the plain forward map's: a payload request runs the exact lane whatever `lane` says
+    pay = np.random.default_rng(0).normal(size=(len(f), 3))
+    x = m.trace_batch(f, b, d, payload=pay, lane="fast")
+    y = m.trace_batch(f, b, d, payload=pay)
+    assert np.array_equal(x.bary, y.bary) and np.array_equal(x.payload, y.payload)
+    # no crossing records on the mesh: nothing for the lane to walk over -> exact bits
+    plain = gpu.Mesh(a["xyz"], a["tri"], transport_cache=False)
+    assert np.array_equal(plain.trace_batch(f, b, d, lane="fast").bary, y.bary)
+    # and where it applies it is the same walk, within tolerance, on a big enough batch for every code path
+    f2, b2, d2 = rm.sample_queries(2, 40000, 0.2, 3.0)
+    ex, fa = m.trace_batch(f2, b2, d2), m.trace_batch(f2, b2, d2, lane="fast")
+    assert np.array_equal(ex.face, fa.face) and np.array_equal(ex.crossings, fa.crossings)
+    assert np.abs(m.embed(ex.face, ex.bary) - m.embed(fa.face, fa.bary)).max() <= 1e-9 * 2.0
