@@ -846,6 +846,7 @@ static int trace_batch_multi_device(const dg_mesh* mesh, int64_t n, const dg_tra
   }
   DG_CUDA(cudaEventRecord(ready, home));
   int rc = DG_OK;
+  std::vector<cudaEvent_t> joins;
   for (int k = 0; k < S && rc == DG_OK; ++k) {
     const Shard& s = shards[size_t(k)];
     if (s.n == 0) continue;
@@ -879,10 +880,13 @@ static int trace_batch_multi_device(const dg_mesh* mesh, int64_t n, const dg_tra
     ps.note(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     if (done) {
       ps.note(cudaEventRecord(done, ws));
-      ps.note(cudaStreamWaitEvent(home, done, 0));
-      cudaEventDestroy(done);   // released once the recorded work has completed
+      joins.push_back(done);   // the caller's stream waits for it below, with the primary device current again
     }
     if (rc == DG_OK && ps.error() != cudaSuccess) rc = fail_cuda(ps.error(), "dg_trace_batch peer copies");
+  }
+  for (cudaEvent_t done : joins) {
+    if (cudaStreamWaitEvent(home, done, 0) != cudaSuccess && rc == DG_OK) rc = fail(DG_ERR_CUDA, "dg_trace_batch: joining the shards");
+    cudaEventDestroy(done);   // released once the recorded work has completed
   }
   cudaEventDestroy(ready);
   if (parts) {
