@@ -448,7 +448,7 @@ class Batch:
             pass
 
     def trace(self, face, bary, dirs, max_steps=0, refill_min=0, blocks_per_sm=0, out=None, gfd=False, eps_v=None,
-              eps_p=None):
+              eps_p=None, lane="exact"):
         """gfd=True: the forward of a step whose backward will be GFD (dg_batch_trace_gfd): the Jacobians are
         computed with the forward traces (fourth sibling of GFD's round 2) and stay on the GPU; the following
         Batch.gfd(g=...) with the same eps only pulls g back."""
@@ -462,7 +462,7 @@ class Batch:
             status=np.empty(n, np.uint8), stall=np.empty(n, np.uint8),
             npoints=np.empty(n, np.int32), crossings=np.empty(n, np.int32))
         cfg = TraceCfg(max_steps=int(max_steps), memory=capi.MEM_HOST, refill_min=int(refill_min),
-                       blocks_per_sm=int(blocks_per_sm))
+                       blocks_per_sm=int(blocks_per_sm), lane=LANES[lane])
         tin = TraceIn(ptr(face), ptr(bary), ptr(dirs), None)
         total = C.c_uint64(0)
         o = TraceOut(ptr(r.face), ptr(r.bary), ptr(r.dir), ptr(r.traced), ptr(r.requested), ptr(r.term),

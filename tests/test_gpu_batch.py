@@ -111,3 +111,33 @@ def test_batch_contract_errors(gpu, ref):
     with pytest.raises(gpu.DgError) as e:
         batch.ep_backward(np.ones((16, 3)))
     assert e.value.klass == "DegenerateDirection" and e.value.index == 5
+
+
+def test_resident_batch_in_the_tolerance_lane(gpu, ref):
+    """dg_trace_cfg.lane = DG_LANE_FAST through the resident batch: forward (plain and as the forward of a GFD step) and
+    the pull-back agree with the exact lane's within the lane's bar -- same end faces, 1e-9 x diagonal, GFD gradients
+    cos >= 0.999999 -- and with the lane's own device-mode calls bit for bit."""
+    rm = ref.RefMesh.torus(1 / 3, 1 / 6, 64, 32)
+    a = rm.arrays()
+    m = gpu.Mesh(a["xyz"], a["tri"])
+    f, b, d = rm.sample_queries(17, 70000, 0.05, 0.9)
+    g = np.random.default_rng(1).normal(size=(len(f), 3))
+    bt = gpu.Batch(m, len(f))
+    exact = bt.trace(f, b, d)
+    fast = bt.trace(f, b, d, lane="fast")
+    direct = m.trace_batch(f, b, d, lane="fast")
+    assert np.array_equal(fast.bary, direct.bary) and np.array_equal(fast.dir, direct.dir)
+    assert np.array_equal(fast.face, exact.face) and not np.array_equal(fast.bary, exact.bary)
+    diag = np.linalg.norm(a["xyz"].max(0) - a["xyz"].min(0))
+    assert np.abs(m.embed(fast.face, fast.bary) - m.embed(exact.face, exact.bary)).max() <= 1e-9 * diag
+    fused = bt.trace(f, b, d, gfd=True, lane="fast")
+    assert np.array_equal(fused.bary, fast.bary)
+    out = bt.gfd(g=g)
+    sep = m.gfd(f, b, d, g=g)
+    for k in ("grad_v", "grad_p"):
+        num = np.einsum("nd,nd->n", out[k], sep[k])
+        den = np.linalg.norm(out[k], axis=1) * np.linalg.norm(sep[k], axis=1)
+        ok = den > 1e-12
+        assert (num[ok] / den[ok]).min() >= 0.999999, k
+    assert np.abs(out["jv"] - sep["jv"]).max() <= 1e-5 * np.abs(sep["jv"]).max()
+    bt.close()
