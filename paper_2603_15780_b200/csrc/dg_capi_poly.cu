@@ -91,6 +91,11 @@ __global__ void __launch_bounds__(1024) poly_scan_compact_small_kernel(const int
   }
 }
 
+// Most points a trace can record: the start point, then one per step (advance, tracer.cpp:202,212) -- two with hole
+// avoidance, where a step that reaches a boundary edge pushes its advance AND the slide that follows it
+// (cross_edge -> slide_from_edge -> slide_along, tracer.cpp:371-405).
+int64_t most_points(int32_t max_steps, bool hole_avoidance) { return (hole_avoidance ? 2 : 1) * int64_t(max_steps) + 2; }
+
 size_t slot_budget() {
   const char* e = getenv("DG_POLY_SLOT_BUDGET");   // points of slot space of pass 1 (36 B each)
   return e ? size_t(std::max<long long>(1024, atoll(e))) : (size_t(8) << 20);
@@ -261,8 +266,9 @@ extern "C" int dg_trace_polylines(const dg_mesh* mesh, int64_t n, const dg_trace
   const size_t N = size_t(n);
   {
     const int32_t steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
-    if (n > 0 && n <= kSmallMax && N * size_t(steps + 2) <= slot_budget())
-      return trace_polylines_small(mesh, n, in, c, out, poly, ps, steps, steps + 2);
+    const int64_t full = most_points(steps, c.hole_avoidance != 0);
+    if (n > 0 && n <= kSmallMax && full <= 0x7fffffff && N * size_t(full) <= slot_budget())
+      return trace_polylines_small(mesh, n, in, c, out, poly, ps, steps, int32_t(full));
   }
   if (ps.offsets_cap < N + 1) {
     const size_t cap = std::max<size_t>(2 * (N + 1), 1024);
@@ -280,8 +286,7 @@ extern "C" int dg_trace_polylines(const dg_mesh* mesh, int64_t n, const dg_trace
   cudaStream_t stream = mesh->stream;
   Stage st(stream, false);
   const int32_t max_steps = c.max_steps > 0 ? c.max_steps : default_max_steps(mesh->nf);
-  // one start point + one point per step at most (a step pushes at most one point, tracer.cpp:202,212,396)
-  const int64_t full_cap = int64_t(max_steps) + 2;
+  const int64_t full_cap = most_points(max_steps, c.hole_avoidance != 0);
   const int32_t cap = int32_t(std::max<int64_t>(8, std::min<int64_t>(full_cap, int64_t(slot_budget() / N))));
   const size_t slots = N * size_t(cap);
 

@@ -373,3 +373,34 @@ def test_new_entry_points_on_empty_and_odd_requests(gpu, ref):
     ex, fa = m.trace_batch(f2, b2, d2), m.trace_batch(f2, b2, d2, lane="fast")
     assert np.array_equal(ex.face, fa.face) and np.array_equal(ex.crossings, fa.crossings)
     assert np.abs(m.embed(ex.face, ex.bary) - m.embed(fa.face, fa.bary)).max() <= 1e-9 * 2.0
+
+
+def test_polyline_slots_hold_two_points_per_step_under_hole_avoidance(gpu, ref):
+    """One-call polylines with hole avoidance under a tight step limit (all three size paths) against the reference."""
+    # hole avoidance under a tight step limit: a step that reaches a boundary edge pushes TWO points (its advance and the
+    # slide along the boundary), so a trace can record up to 2 max_steps + 2 points -- the slots must hold them
+    # (found by scripts/fuzz_walkers.py: "a trace recorded more points than its step limit allows")
+    rng = np.random.default_rng(5)
+    nx, ny = 12, 9
+    gx, gy = np.meshgrid(np.arange(nx + 1.0), np.arange(ny + 1.0), indexing="ij")
+    xyz = np.stack([gx.ravel(), gy.ravel(), np.zeros(gx.size)], 1)
+    xyz[:, :2] += 0.3 * rng.uniform(-0.5, 0.5, (len(xyz), 2))      # jittered open grid
+    idx = lambda i, j: i * (ny + 1) + j
+    tri = np.array([[idx(i, j), idx(i + 1, j), idx(i + 1, j + 1)] for i in range(nx) for j in range(ny)] +
+                   [[idx(i, j), idx(i + 1, j + 1), idx(i, j + 1)] for i in range(nx) for j in range(ny)], np.int32)
+    gm, gr = gpu.Mesh(xyz, tri), ref.RefMesh.build(xyz, tri)
+    from paper_2603_15780_b200 import workloads as W
+    diag = W.bbox_diagonal(xyz)
+    f, b, d = W.sample_queries(xyz, tri, 30000, (0.5 * diag, 3 * diag), seed=3)
+    for steps in (5, 60):
+        r = gr.trace_batch(f, b, d, record_polyline=True, hole_avoidance=True, max_steps=steps)
+        hot = np.nonzero(r.npoints > steps + 2)[0]
+        assert len(hot) > 0                                          # the case is in the batch
+        a = gm.trace_batch(f, b, d, record_polyline=True, hole_avoidance=True, max_steps=steps)     # large path
+        assert_trace_equal(r, a, len(f))
+        sub = np.concatenate([hot, np.arange(1000)])                 # one-block small path (<= 2 048 traces)
+        a = gm.trace_batch(f[sub], b[sub], d[sub], record_polyline=True, hole_avoidance=True, max_steps=steps)
+        rs = gr.trace_batch(f[sub], b[sub], d[sub], record_polyline=True, hole_avoidance=True, max_steps=steps)
+        assert_trace_equal(rs, a, len(sub))
+        a = gm.trace_batch(f[sub[:200]], b[sub[:200]], d[sub[:200]], record_polyline=True, hole_avoidance=True, max_steps=steps)   # mapped
+        assert np.array_equal(a.poly_bary, rs.poly_bary[:rs.poly_offsets[200]])
