@@ -260,7 +260,15 @@ cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, La
   // the fast walker carries the payload along, writes one polyline point per step and leaves boundary
   // events to the full Tracer behind it
   const bool payload_only = (p.payload || p.o_payload || p.hole_avoidance || p.poly_offsets || p.poly_cap > 0) && !p.want_q && !p.o_transport;
-  if (payload_only && shape.walker != 1 && fast_walk_enabled()) return fast(std::integral_constant<int, 1>{});
+  if (payload_only && shape.walker != 1 && fast_walk_enabled()) {
+    // no payload to carry (the reference's default call: record_polyline = true, no payload): the polyline-only
+    // instantiation -- the plain walker's step plus one polyline point (TMA requests take the cooperative gather)
+    if (!p.payload && !p.o_payload) {
+      if (!p.mesh.he) return launch_fast<false, 0, 3>(p, shape, stream);
+      return gather != 0 ? launch_fast<true, 2, 3>(p, shape, stream) : launch_fast<true, 0, 3>(p, shape, stream);
+    }
+    return fast(std::integral_constant<int, 1>{});
+  }
   // the transport matrix as well: three more vectors through every fold isometry
   if (p.want_q && shape.walker != 1 && fast_walk_enabled()) return fast(std::integral_constant<int, 2>{});
   if (p.mesh.he) return needs_full ? launch_one<double, true, true>(p, shape, stream) : launch_one<double, false, true>(p, shape, stream);
