@@ -26,6 +26,15 @@ struct dg_batch {
   uint8_t *o_term = nullptr, *o_status = nullptr, *o_stall = nullptr;
   uint64_t* totals = nullptr;  // [kStreams] per-slice crossing counts / EP error words (device)
   uint64_t* words = nullptr;   // [kStreams] pinned host mirror (a pageable target would make the copy block)
+  // streamed forward (batch_trace_streamed): upload cursor, per-chunk completion counts and error word on the device,
+  // chunk flags and the cursor's values in pinned host memory
+  static constexpr int kChunkShift = 14;   // smallest chunk (sizes the arrays); the request picks its own
+  unsigned long long* up_word = nullptr;
+  unsigned int* chunk_done = nullptr;      // [chunks + 1]: the last word is the error word
+  unsigned int* chunk_flags = nullptr;     // pinned, mapped
+  unsigned long long* up_table = nullptr;  // pinned: end index of every chunk
+  unsigned long long* ctr = nullptr;       // device [2]: work cursor, crossing total
+  cudaEvent_t ev_zero = nullptr;
   // backward
   double *g = nullptr, *grad_v = nullptr, *grad_p = nullptr, *jv = nullptr, *jp = nullptr;
   uint8_t* degraded = nullptr;
@@ -113,6 +122,13 @@ int dgapi::batch_create_one(const dg_mesh* mesh, int64_t capacity, dg_batch** ou
   ok(dev_alloc(&b->o_npoints, N)); ok(dev_alloc(&b->o_crossings, N));
   ok(dev_alloc(&b->totals, size_t(dg_batch::kStreams)));
   ok(cudaMallocHost(reinterpret_cast<void**>(&b->words), dg_batch::kStreams * sizeof(uint64_t)));
+  {
+    const size_t chunks = (N >> dg_batch::kChunkShift) + 1;
+    ok(dev_alloc(&b->up_word, 1)); ok(dev_alloc(&b->chunk_done, chunks + 1)); ok(dev_alloc(&b->ctr, 2));
+    ok(cudaMallocHost(reinterpret_cast<void**>(&b->chunk_flags), chunks * sizeof(unsigned int)));
+    ok(cudaMallocHost(reinterpret_cast<void**>(&b->up_table), chunks * sizeof(unsigned long long)));
+    ok(cudaEventCreateWithFlags(&b->ev_zero, cudaEventDisableTiming));
+  }
   // (the backward buffers g / grad_v / grad_p are allocated by the first backward call: a forward-only user --
   // the resident batch behind large DG_MEM_HOST dg_trace_batch calls -- never pays for them)
   if (e != cudaSuccess) {
@@ -137,6 +153,10 @@ void dg_batch_destroy(dg_batch* b) {
   cudaFree(b->o_traced); cudaFree(b->o_requested); cudaFree(b->o_term); cudaFree(b->o_status); cudaFree(b->o_stall);
   cudaFree(b->o_npoints); cudaFree(b->o_crossings); cudaFree(b->totals);
   if (b->words) cudaFreeHost(b->words);
+  cudaFree(b->up_word); cudaFree(b->chunk_done); cudaFree(b->ctr);
+  if (b->chunk_flags) cudaFreeHost(b->chunk_flags);
+  if (b->up_table) cudaFreeHost(b->up_table);
+  if (b->ev_zero) cudaEventDestroy(b->ev_zero);
   cudaFree(b->g); cudaFree(b->grad_v); cudaFree(b->grad_p); cudaFree(b->jv); cudaFree(b->jp); cudaFree(b->degraded);
   delete b;
 }
@@ -144,6 +164,101 @@ void dg_batch_destroy(dg_batch* b) {
 int64_t dg_batch_size(const dg_batch* b) { return b && b->traced ? (b->shards.empty() ? b->n : b->n_total) : 0; }
 
 }  // extern "C"
+
+// The streamed forward: ONE walker over the whole request while its queries arrive and its results leave.
+//   copy-in stream   the queries in pieces (2^15, 2^15, 2^16, 2^17, then 2^18 each), the upload cursor advanced
+//                    behind every piece;
+//   walker stream    one persistent launch at full occupancy; a warp takes work only below the upload cursor, every
+//                    finished trace is counted into its chunk of 32 768 and the one that completes a chunk raises
+//                    the chunk's flag in mapped host memory (dg_fast_walk.cuh, kStream);
+//   this thread      waits for the flags in order and queues the finished chunks' results on the copy-out stream.
+// Against the sliced pipeline below (a walker per slice) nothing ramps up or drains between slices, the walker
+// starts after 1.7 MB instead of a tenth of the request, and the device-to-host tail is what was still in flight
+// when the queue ran dry instead of the last slice. c2, 1 M geodesics through pinned buffers: 4.06 ms against 4.48
+// sliced (walker alone 3.61; the streamed walker 3.77: listing and counting the finished traces; ~0.06 ms until
+// the first queries are there; ~0.2 ms of copies after the last trace). Plain order only: a schedule in start-face
+// order finishes its traces all over the request. Same step code, same bits (tests/test_gpu_batch.py).
+// DG_BATCH_STREAM=0 or DG_BATCH_SLICES=k selects the sliced pipeline.
+static bool stream_enabled() {
+  static const bool on = [] { const char* e = getenv("DG_BATCH_STREAM"); return !(e && e[0] == '0'); }();
+  return on;
+}
+static int batch_trace_streamed(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg& c, dg_trace_out* out,
+                                const dg::TraceParams& p_in, dg::LaunchShape shape) {
+  // completion is counted per chunk of 32 768 traces (DG_BATCH_CHUNK_SHIFT); the copies are coarser where it costs
+  // nothing: a copy call is ~4 us of this thread, and only the last chunks are on the critical path
+  static const int sh = [] { const char* e = getenv("DG_BATCH_CHUNK_SHIFT"); return e ? std::max(int(dg_batch::kChunkShift), std::min(24, atoi(e))) : 15; }();
+  const int64_t chunk = int64_t(1) << sh;
+  const int K = int((n + chunk - 1) >> sh);
+  cudaStream_t s_in = b->streams[0], s_walk = b->streams[1], s_out = b->streams[2];
+  cudaError_t e = cudaSuccess;
+  auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  for (int k = 0; k < K; ++k) b->chunk_flags[k] = 0u;
+  // queries [lo, hi) in, then the upload cursor to hi (its values live in pinned memory until the copy has run)
+  int ups = 0;
+  auto upload = [&](int64_t lo, int64_t hi) {
+    const size_t L = size_t(lo), M = size_t(hi - lo);
+    note(cudaMemcpyAsync(b->face + L, in->face + L, M * 4, cudaMemcpyHostToDevice, s_in));
+    note(cudaMemcpyAsync(b->bary + 3 * L, in->bary + 3 * L, M * 24, cudaMemcpyHostToDevice, s_in));
+    note(cudaMemcpyAsync(b->dir + 3 * L, in->dir + 3 * L, M * 24, cudaMemcpyHostToDevice, s_in));
+    b->up_table[ups] = (unsigned long long)hi;
+    note(cudaMemcpyAsync(b->up_word, b->up_table + ups, sizeof(unsigned long long), cudaMemcpyHostToDevice, s_in));
+    ++ups;
+  };
+  note(cudaMemsetAsync(b->up_word, 0, sizeof(unsigned long long), s_in));
+  note(cudaEventRecord(b->ev_zero, s_in));
+  // a small first piece starts the walker early; the rest arrives in a few large pieces (the link is ~4 x faster
+  // than the walker consumes queries)
+  const int64_t first = std::min<int64_t>(n, int64_t(1) << 15), piece = int64_t(1) << 18;
+  upload(0, first);
+  dg::TraceParams p = p_in;
+  p.queue_head = b->ctr;
+  p.total_crossings = b->ctr + 1;
+  p.stream_uploaded = b->up_word;
+  p.stream_done = b->chunk_done;
+  p.stream_error = b->chunk_done + K;
+  p.stream_flags = b->chunk_flags;
+  p.stream_shift = sh;
+  note(cudaMemsetAsync(b->ctr, 0, 2 * sizeof(unsigned long long), s_walk));
+  note(cudaMemsetAsync(b->chunk_done, 0, size_t(K + 1) * sizeof(unsigned int), s_walk));
+  note(cudaStreamWaitEvent(s_walk, b->ev_zero, 0));
+  note(dg::launch_trace_streamed(p, shape, s_walk));
+  b->words[1] = 0;
+  note(cudaMemcpyAsync(&b->words[0], b->ctr + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s_walk));
+  note(cudaMemcpyAsync(&b->words[1], b->chunk_done + K, sizeof(unsigned int), cudaMemcpyDeviceToHost, s_walk));
+  // pieces of 2^15, 2^15, 2^16, 2^17, then 2^18 queries: the resident lanes all have work within ~0.1 ms
+  for (int64_t lo = first; lo < n;) { const int64_t len = std::min(piece, lo); upload(lo, std::min(n, lo + len)); lo += len; }
+  if (e == cudaSuccess) {
+    const volatile unsigned int* flags = b->chunk_flags;
+    bool walker_gone = false;
+    // results out: four chunks per copy while the walker has most of its work ahead, chunk by chunk over the last 2^18
+    const int fine_from = std::max(0, K - int((int64_t(1) << 18) >> sh));
+    for (int k = 0; k < K;) {
+      const int group = k < fine_from ? std::min(4, fine_from - k) : 1;
+      for (int j = k; j < k + group; ++j)
+        for (unsigned spins = 0; !flags[j] && !walker_gone; ++spins)
+          if ((spins & 1023u) == 1023u && cudaStreamQuery(s_walk) != cudaErrorNotReady) walker_gone = true;   // ended (or failed) without the flag
+      if (walker_gone) note(cudaStreamSynchronize(s_walk));   // (its writes are complete before anything is copied)
+      const size_t L = size_t(k) << sh, M = size_t(std::min<int64_t>(chunk * group, n - int64_t(L)));
+      auto back = [&](auto* host, const auto* dev, size_t stride) {
+        if (host) note(cudaMemcpyAsync(host + stride * L, dev + stride * L, M * stride * sizeof(*host), cudaMemcpyDeviceToHost, s_out));
+      };
+      back(out->bary, b->o_bary, 3); back(out->dir, b->o_dir, 3); back(out->face, b->o_face, 1);
+      back(out->traced, b->o_traced, 1); back(out->requested, b->o_requested, 1);
+      back(out->term, b->o_term, 1); back(out->status, b->o_status, 1); back(out->stall, b->o_stall, 1);
+      back(out->npoints, b->o_npoints, 1); back(out->crossings, b->o_crossings, 1);
+      k += group;
+    }
+  }
+  note(cudaStreamSynchronize(s_in));
+  note(cudaStreamSynchronize(s_walk));
+  note(cudaStreamSynchronize(s_out));
+  if (e != cudaSuccess) return fail_cuda(e, "dg_batch_trace (streamed)");
+  if (uint32_t(b->words[1]) != 0u) return fail(DG_ERR_CUDA, "dg_batch_trace: the walker gave up waiting for its queries");
+  if (out->total_crossings) *out->total_crossings = b->words[0];
+  b->traced = true;
+  return DG_OK;
+}
 
 // Forward exp map of n host-resident queries. The request is cut into slices on separate streams:
 // the H2D copy of slice i+1 and the D2H copy of slice i-1 overlap the walker of slice i.
@@ -172,6 +287,27 @@ int dgapi::batch_trace_one(dg_batch* b, int64_t n, const dg_trace_in* in, const 
     return DG_OK;
   }
   const int S = slices_for(n);
+  if (S >= 4 && stream_enabled() && c.sort_by_face != DG_SORT_ON && !getenv("DG_BATCH_SLICES")) {
+    // the streamed form, when this request would run in plain order on the instantiation that has one
+    dg::TraceParams p{};
+    b->mesh->bind(p);
+    p.n = n;
+    p.face = b->face; p.bary = b->bary; p.dir = b->dir;
+    p.o_face = b->o_face; p.o_bary = b->o_bary; p.o_dir = b->o_dir; p.o_traced = b->o_traced; p.o_requested = b->o_requested;
+    p.o_term = b->o_term; p.o_status = b->o_status; p.o_stall = b->o_stall;
+    p.o_npoints = out->npoints ? b->o_npoints : nullptr;
+    p.o_crossings = out->crossings ? b->o_crossings : nullptr;
+    p.max_steps = b->traced_max_steps;
+    p.refill_min = c.refill_min;
+    p.lane_fast = c.lane == DG_LANE_FAST;
+    const dg::LaunchShape shape{b->mesh->sm_count, int(c.blocks_per_sm), int(c.walker)};
+    dg_trace_cfg probe = c;
+    probe.memory = DG_MEM_DEVICE;
+    int face_order = 0, gather = 0;
+    if (dg_trace_plan(b->mesh, n, &probe, &face_order, &gather) == DG_OK && !face_order &&
+        dg::trace_streamable(p, c.use_f32 != 0, false, shape))
+      return batch_trace_streamed(b, n, in, c, out, p, shape);
+  }
   cudaError_t e = cudaSuccess;
   auto note = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   int rc = DG_OK;

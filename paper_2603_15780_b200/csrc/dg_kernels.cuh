@@ -63,6 +63,16 @@ struct TraceParams {
   uint8_t want_q;
   uint8_t he_map_ok;  // he_map is a valid tensor map of mesh.he
   uint8_t lane_fast;  // DG_LANE_FAST: plain forward requests over crossing records run the tolerance lane
+  // Streamed request (launch_trace_streamed; plain order only): the queries arrive and the results leave WHILE the
+  // walker runs. The copy stream that uploads the queries chunk by chunk advances *stream_uploaded behind every
+  // chunk; a warp takes work only below it. Every finished trace counts into its chunk (1 << stream_shift
+  // queries), and the trace that completes a chunk raises the chunk's flag in mapped host memory -- the host
+  // then copies that chunk's results back while the walker goes on.
+  const unsigned long long* stream_uploaded;
+  unsigned int* stream_done;    // [chunks] device
+  unsigned int* stream_flags;   // [chunks] mapped pinned host memory
+  unsigned int* stream_error;   // device: set when the wait for queries gave up (the copy stream failed)
+  int32_t stream_shift;
 };
 
 struct LaunchShape {
@@ -74,6 +84,12 @@ struct LaunchShape {
 // needs_full: any of payload / transport matrix / hole avoidance / polyline is requested.
 cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
                          cudaStream_t stream);
+
+// The streamed form of the plain f64 forward launch (TraceParams::stream_*). trace_streamable: whether launch_trace
+// would run this request on the instantiation that has a streamed twin (crossing records, per-lane loads, exact
+// lane, plain order).
+bool trace_streamable(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape);
+cudaError_t launch_trace_streamed(const TraceParams& p, LaunchShape shape, cudaStream_t stream);
 
 // Whether the fast walker gathers this mesh's crossing records through TMA (AUTO policy).
 // gather of the crossing records for a lone-trace batch on this mesh: 0 per-lane loads, 1 TMA, 2 cooperative loads

@@ -160,7 +160,7 @@ cudaError_t launch_one(const TraceParams& p_in, LaunchShape shape, cudaStream_t 
   return cudaGetLastError();
 }
 
-template <bool kCached, int kTma, int kPay = 0, bool kDense = false, int kLane = 0>
+template <bool kCached, int kTma, int kPay = 0, bool kDense = false, int kLane = 0, bool kStream = false>
 cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t stream) {
   constexpr size_t smem = kTma ? size_t(kFastTmaSmemBytes) : 0;
   TraceParams p = p_in;
@@ -173,7 +173,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
     static std::atomic<int> cached_per_sm{0};
     per_sm = cached_per_sm.load(std::memory_order_relaxed);
     if (per_sm <= 0) {
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma, kPay, kDense, kLane>, DG_FAST_BLOCK, smem);
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_fast_kernel<kCached, kTma, kPay, kDense, kLane, kStream>, DG_FAST_BLOCK, smem);
       if (e != cudaSuccess) return e;
       if (per_sm < 1) per_sm = 1;
       cached_per_sm.store(per_sm, std::memory_order_relaxed);
@@ -183,7 +183,7 @@ cudaError_t launch_fast(const TraceParams& p_in, LaunchShape shape, cudaStream_t
   const long long needed = (p.n + DG_FAST_BLOCK - 1) / DG_FAST_BLOCK;
   if (blocks > needed) blocks = needed;
   if (blocks < 1) blocks = 1;
-  trace_fast_kernel<kCached, kTma, kPay, kDense, kLane><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
+  trace_fast_kernel<kCached, kTma, kPay, kDense, kLane, kStream><<<unsigned(blocks), DG_FAST_BLOCK, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
@@ -228,6 +228,16 @@ int gather_mode(const MeshView& m, int siblings, bool map_ok, int walker, bool f
 }  // namespace
 
 int fast_walker_gather_mode(const MeshView& m, bool map_ok, bool face_order) { return fast_walk_enabled() ? gather_mode(m, 0, map_ok, 0, face_order) : 0; }
+
+bool trace_streamable(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape) {
+  return !use_f32 && !needs_full && shape.walker != 1 && fast_walk_enabled() && !p.lane_fast && p.mesh.he && !p.perm &&
+         p.siblings <= 1 && p.aux_from == 0 && gather_mode(p.mesh, p.siblings, p.he_map_ok != 0, shape.walker, false) == 0;
+}
+cudaError_t launch_trace_streamed(const TraceParams& p, LaunchShape shape, cudaStream_t stream) {
+  if (p.n <= 0) return cudaSuccess;
+  if (!p.stream_uploaded || !p.stream_done || !p.stream_flags || !p.stream_error || p.stream_shift < 5) return cudaErrorInvalidValue;
+  return launch_fast<true, 0, 0, false, 0, true>(p, shape, stream);
+}
 
 cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
                          cudaStream_t stream) {

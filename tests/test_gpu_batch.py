@@ -141,3 +141,44 @@ def test_resident_batch_in_the_tolerance_lane(gpu, ref):
         assert (num[ok] / den[ok]).min() >= 0.999999, k
     assert np.abs(out["jv"] - sep["jv"]).max() <= 1e-5 * np.abs(sep["jv"]).max()
     bt.close()
+
+
+def test_streamed_forward_gives_the_bits_of_the_sliced_pipeline(gpu, ref, monkeypatch):
+    """>= 2^18 queries in plain order run as ONE walker while the queries arrive and the results leave (upload cursor,
+    per-chunk completion flags). Same bits as the sliced pipeline and the reference; covers a ragged last chunk,
+    rejected starts, zero-length requests and vertex starts (every way a trace can end), then EP on the resident batch."""
+    rm = ref.RefMesh.icosphere(5)
+    m = gpu_mesh(gpu, rm)
+    n = 4 * 65536 + 40017
+    f, b, d = rm.sample_queries(3, n, 0.01, 1.2)
+    f[5] = -1; f[70000] = rm.nf + 3          # rejected starts
+    d[9] = 0.0; d[131072] = 0.0              # zero-length requests
+    b[11] = [1.0, 0.0, 0.0]; b[200001] = [0.0, 1.0, 0.0]   # vertex starts
+    b[13] = [0.7, 0.7, -0.4]                 # rejected barycentrics
+    batch = gpu.Batch(m, n)
+    for rep in range(2):                     # twice: the counters and flags of the batch are reused
+        h = batch.trace(f, b, d)
+    monkeypatch.setenv("DG_BATCH_SLICES", "4")
+    s = batch.trace(f, b, d)
+    monkeypatch.delenv("DG_BATCH_SLICES")
+    for k in ("face", "bary", "dir", "traced", "requested", "term", "status", "stall", "npoints", "crossings"):
+        assert np.array_equal(getattr(h, k), getattr(s, k)), k
+    assert h.total_crossings == s.total_crossings == int(h.crossings.sum())
+    k = 30000
+    sel = np.r_[100:k, n - k:n]              # (clear of the doctored entries: the reference leaves rejected slots unset,
+                                             # and a vertex start goes through atan2, CUDA's against glibc's)
+    r = rm.trace_batch(f[sel], b[sel], d[sel], record_polyline=True)
+    for name in ("face", "bary", "dir", "traced", "term", "status"):
+        assert np.array_equal(getattr(r, name), getattr(h, name)[sel]), name
+    # EP on a streamed resident batch (clean samples: EP rejects a zero direction for the whole call)
+    f2, b2, d2 = f[100:], b[100:].copy(), d[100:].copy()
+    bad = (np.abs(d2).sum(1) == 0) | (f2 < 0) | (f2 >= rm.nf)
+    f2, b2, d2 = f2[~bad], b2[~bad], d2[~bad]
+    h2 = batch.trace(f2, b2, d2)
+    g = unit_rows(np.random.default_rng(1), len(f2))
+    gv = batch.ep_backward(g)
+    sep = m.ep_backward(f2[:5000], d2[:5000], h2.face[:5000], h2.dir[:5000], g[:5000])
+    assert np.array_equal(gv[:5000], sep)
+    # the host-mode dg_trace_batch of a large plain request runs on the same pipeline
+    t = m.trace_batch(f, b, d)
+    assert np.array_equal(t.bary, h.bary) and np.array_equal(t.face, h.face)
