@@ -280,12 +280,14 @@ typedef struct dg_diff_cfg {
   uint8_t lane;         /* DG_LANE_*: arithmetic of GFD's full-length traces */
   uint8_t schedule;     /* GFD round 2: DG_GFD_SCHEDULE_AUTO = the full-length re-traces of a sample run as
                            sibling lanes of one warp and share every crossing-record fetch;
-                           DG_GFD_SCHEDULE_PLAIN = job order. A schedule only: same bits either way. */
+                           DG_GFD_SCHEDULE_PLAIN = job order; DG_GFD_SCHEDULE_FACE_ORDER = sibling groups handed
+                           out in start-face order of their samples (what AUTO does for >= 32 768 samples on a
+                           mesh whose crossing records exceed the L2). A schedule only: same bits either way. */
   uint8_t reserved[5];
   void* stream;
   int32_t max_steps;    /* GFD re-traces; 0 = default */
 } dg_diff_cfg;
-enum { DG_GFD_SCHEDULE_AUTO = 0, DG_GFD_SCHEDULE_PLAIN = 1 };
+enum { DG_GFD_SCHEDULE_AUTO = 0, DG_GFD_SCHEDULE_PLAIN = 1, DG_GFD_SCHEDULE_FACE_ORDER = 2 };
 
 /* Extrinsic-proxy Jacobians for n samples. rot[9n] = rotation_ep (row-major), frames
  * [DG_FRAME_DOUBLES n]; either may be NULL. Fails with DG_ERR_DEGENERATE_DIRECTION (and

@@ -300,7 +300,8 @@ class Mesh:
                                    ptr(g), C.addressof(cfg), ptr(grad_v), ptr(grad_p), C.addressof(ei)), ei)
 
     def gfd(self, face, bary, v, eps_v=None, eps_p=None, g=None, max_steps=0, out=None, base=None, plain_schedule=False):
-        """gfd_batched_many (+ pullback_ambient when g is given), diff.cpp:273-326. `out`: a dict
+        """gfd_batched_many (+ pullback_ambient when g is given), diff.cpp:273-326. plain_schedule: False = AUTO,
+        True = plain job order, 2 = sibling groups in start-face order of their samples (dg_diff_cfg.schedule). `out`: a dict
         of preallocated (e.g. pinned) arrays; only the keys present are computed and copied back
         (jv, jp, degraded, frames, grad_v, grad_p, base_face, base_bary, base_dir)."""
         h = self._handle()

@@ -132,8 +132,32 @@ __global__ void sort_keys_kernel(const int32_t* __restrict__ face, const double*
 
 // dg_trace_cfg.sort_by_face resolved for a request of n queries
 static bool schedules_by_face(const dg_mesh* mesh, int64_t n, const dg_trace_cfg& c, bool record) {
-  const bool big_mesh = mesh->he && size_t(3) * size_t(mesh->nf) * sizeof(dg::HalfEdgeRec) > (size_t(96) << 20);
+  const bool big_mesh = beyond_l2(mesh);
   return c.sort_by_face == DG_SORT_ON || (c.sort_by_face == DG_SORT_AUTO && big_mesh && n >= (int64_t(1) << 15) && !record);
+}
+
+// The permutation that lists n device-resident queries in start-face order (vertex starts last), in staging of
+// the call; null when the staging could not be had (the request then runs in plain order).
+const int32_t* dgapi::start_face_order(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, Stage& st,
+                                       cudaStream_t stream) {
+  const size_t N = size_t(n);
+  int32_t* keys_in = st.scratch<int32_t>(N);
+  int32_t* keys_out = st.scratch<int32_t>(N);
+  int32_t* iota = st.scratch<int32_t>(N);
+  int32_t* perm = st.scratch<int32_t>(N);
+  if (!keys_in || !keys_out || !iota || !perm) return nullptr;
+  int bits = 1;
+  while ((int64_t(1) << bits) < int64_t(mesh->nf) && bits < 30) ++bits;
+  sort_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(face, bary, n, mesh->nf, bits, keys_in, iota);
+  size_t tmp_bytes = 0;
+  st.note(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, iota, perm, int(n), 0, bits + 1, stream));
+  void* tmp = st.scratch<char>(tmp_bytes);
+  if (!tmp) return nullptr;
+  st.note(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, iota, perm, int(n), 0, bits + 1, stream));
+  return perm;
+}
+bool dgapi::beyond_l2(const dg_mesh* mesh) {
+  return mesh->he && size_t(3) * size_t(mesh->nf) * sizeof(dg::HalfEdgeRec) > (size_t(96) << 20);
 }
 
 void dgapi::ensure_he64(const dg_mesh* m) {
@@ -697,22 +721,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   // c2, L2-resident: +-1 %, stays off). The face order of the mesh is the caller's: a locality-preserving
   // numbering (grid, Morton, Hilbert) is what makes neighbours in the queue neighbours on the surface.
   const bool sort = schedules_by_face(mesh, n, c, record);
-  if (sort) {
-    int32_t* keys_in = st.scratch<int32_t>(N);
-    int32_t* keys_out = st.scratch<int32_t>(N);
-    int32_t* iota = st.scratch<int32_t>(N);
-    int32_t* perm = st.scratch<int32_t>(N);
-    if (keys_in && keys_out && iota && perm) {
-      int bits = 1;
-      while ((int64_t(1) << bits) < int64_t(mesh->nf) && bits < 30) ++bits;
-      sort_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(p.face, p.bary, n, mesh->nf, bits, keys_in, iota);
-      size_t tmp_bytes = 0;
-      st.note(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, iota, perm, int(n), 0, bits + 1, stream));
-      void* tmp = st.scratch<char>(tmp_bytes);
-      if (tmp) st.note(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, iota, perm, int(n), 0, bits + 1, stream));
-      p.perm = perm;
-    }
-  }
+  if (sort) p.perm = start_face_order(mesh, n, p.face, p.bary, st, stream);
   if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_trace_batch staging");
 
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || record ||

@@ -255,6 +255,12 @@ class PeerStage {
   std::vector<Back> backs_;
 };
 
+// Start-face scheduling (dg_capi.cu): whether the mesh's crossing records exceed what the L2 holds, and the
+// permutation that lists n device-resident queries in start-face order (null: staging failed, run in plain order).
+bool beyond_l2(const dg_mesh* mesh);
+const int32_t* start_face_order(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, Stage& st,
+                                cudaStream_t stream);
+
 void poly_store_free(dg_poly_store* s);
 // Builds the half-size records of the tolerance lane on first use (no-op afterwards; quietly leaves he64 null when
 // the mesh has no crossing records or the memory is not there: the lane then runs over the 128-byte records).

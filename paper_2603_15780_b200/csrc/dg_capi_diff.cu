@@ -26,7 +26,8 @@ struct AuxOut {
 cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const double* jb, const double* jd,
                      const double* jp, int32_t* rf, double* rb, double* rd, double* rp, uint8_t* rt, uint8_t* rs,
                      int max_steps, unsigned long long* total, cudaStream_t stream, unsigned long long* cursor,
-                     int siblings = 0, int64_t sibling_stride = 0, const AuxOut* aux = nullptr, bool lane_fast = false) {
+                     int siblings = 0, int64_t sibling_stride = 0, const AuxOut* aux = nullptr, bool lane_fast = false,
+                     const int32_t* sample_order = nullptr) {
   if (n <= 0) return cudaSuccess;
   dg::TraceParams p{};
   mesh->bind(p);
@@ -36,6 +37,7 @@ cudaError_t run_jobs(const dg_mesh* mesh, int64_t n, const int32_t* jf, const do
   p.max_steps = max_steps;
   p.refill_min = 0;  // the walker's own default
   p.siblings = siblings; p.sibling_stride = sibling_stride;
+  p.perm = siblings > 1 ? sample_order : nullptr;   // with a sibling schedule: the order of the GROUPS (samples)
   p.lane_fast = lane_fast;   // (payload-carrying launches run the exact lane whatever this says)
   if (aux) {
     p.aux_from = aux->from;
@@ -480,12 +482,19 @@ int dgapi::gfd_jacobians_impl(const dg_mesh* mesh, int64_t n, const int32_t* fac
   // round 2: the full-length jobs of every sample as one sibling group
   st.note(dg::launch_gfd_round2_jobs(b, stream));
   const int group = c.schedule == DG_GFD_SCHEDULE_PLAIN ? 0 : gfd_siblings();
+  // On meshes beyond the L2 the sibling groups are handed out in start-face order of their samples, like lone
+  // traces are (dg_trace_cfg.sort_by_face): samples that start side by side walk through the same neighbourhood
+  // at the same time. A schedule only -- every job writes at its own index.
+  const int32_t* order = nullptr;
+  if (group && (c.schedule == DG_GFD_SCHEDULE_FACE_ORDER ||
+                (beyond_l2(mesh) && n >= (int64_t(1) << 15) && !std::getenv("DG_GFD_PLAIN_SAMPLE_ORDER"))))
+    order = start_face_order(mesh, n, b.face, b.bary, st, stream);
   if (known_base) {
     st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, nullptr, nullptr,
-                     b.r2_term, b.r2_status, max_steps, nullptr, stream, cursors + 1, group ? 3 : 0, n, nullptr, lane_fast));
+                     b.r2_term, b.r2_status, max_steps, nullptr, stream, cursors + 1, group ? 3 : 0, n, nullptr, lane_fast, order));
   } else {
     st.note(run_jobs(mesh, 4 * n, b.j2_face, b.j2_bary, b.j2_dir, nullptr, b.r2_face, b.r2_bary, r2_dir, nullptr,
-                     b.r2_term, b.r2_status, max_steps, fwd_total, stream, cursors + 1, group ? 4 : 0, n, fwd ? &aux : nullptr, lane_fast));
+                     b.r2_term, b.r2_status, max_steps, fwd_total, stream, cursors + 1, group ? 4 : 0, n, fwd ? &aux : nullptr, lane_fast, order));
     st.note(dg::launch_gfd_par_jobs(b, stream));
     st.note(run_jobs(mesh, n, b.par_jface, b.par_jbary, b.par_jdir, nullptr, par_rface, par_rbary, nullptr, nullptr,
                      par_rterm, par_rstatus, max_steps, nullptr, stream, cursors + 2));

@@ -49,7 +49,7 @@ struct TraceParams {
   unsigned long long* total_crossings;  // optional: += sum of crossings of the batch
   int32_t max_steps;
   int32_t refill_min;  // refill a warp once this many lanes are idle (0 = the walker's default)
-  // Sibling schedule (perm must be null): the first siblings * sibling_stride elements of the schedule are
+  // Sibling schedule (perm, if given, orders the GROUPS: stride entries): the first siblings * sibling_stride elements of the schedule are
   // groups of `siblings` queries {g, g + stride, ..., g + (siblings-1) stride}, handed to lanes of ONE warp
   // together. GFD's re-traces of one sample follow the same faces step for step, so the group gathers the
   // same crossing records at the same time: one HBM / L2 line serves all of them. 0 / 1 = plain order.

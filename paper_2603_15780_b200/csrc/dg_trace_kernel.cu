@@ -239,9 +239,15 @@ cudaError_t launch_trace_streamed(const TraceParams& p, LaunchShape shape, cudaS
   return launch_fast<true, 0, 0, false, 0, true>(p, shape, stream);
 }
 
-cudaError_t launch_trace(const TraceParams& p, bool use_f32, bool needs_full, LaunchShape shape,
+cudaError_t launch_trace(const TraceParams& p_in, bool use_f32, bool needs_full, LaunchShape shape,
                          cudaStream_t stream) {
-  if (p.n <= 0) return cudaSuccess;
+  if (p_in.n <= 0) return cudaSuccess;
+  // The general walker has no sibling schedule: it runs such a request in plain order (and the order of the GROUPS
+  // that perm then holds means nothing to it).
+  TraceParams plain = p_in;
+  if (plain.siblings > 1) plain.perm = nullptr;
+  const bool general = use_f32 || shape.walker == 1 || !fast_walk_enabled();
+  const TraceParams& p = general ? plain : p_in;
   if (use_f32) {
     return needs_full ? launch_one<float, true, false>(p, shape, stream) : launch_one<float, false, false>(p, shape, stream);
   }

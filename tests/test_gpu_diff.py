@@ -123,7 +123,10 @@ def test_gfd_sibling_schedule_and_known_base_change_no_bit(gpu, ref, cache):
         g = unit_rows(np.random.default_rng(3), len(f))
         kw = dict(g=g) if eps is None else dict(g=g, eps_v=eps, eps_p=eps)
         want = m.gfd(f, b, d, plain_schedule=True, **kw)
-        for got in (m.gfd(f, b, d, **kw), m.gfd(f, b, d, base=base, **kw), m.gfd(f, b, d, base=base, plain_schedule=True, **kw)):
+        # plain_schedule = 2: DG_GFD_SCHEDULE_FACE_ORDER, the sibling groups in start-face order of their samples
+        # (groups of 4, and groups of 3 + a plain tail with a known base)
+        for got in (m.gfd(f, b, d, **kw), m.gfd(f, b, d, base=base, **kw), m.gfd(f, b, d, base=base, plain_schedule=True, **kw),
+                    m.gfd(f, b, d, plain_schedule=2, **kw), m.gfd(f, b, d, base=base, plain_schedule=2, **kw)):
             for k in ("jv", "jp", "degraded", "frames", "grad_v", "grad_p"):
                 assert np.array_equal(got[k], want[k], equal_nan=True), k
         if eps is not None:

@@ -47,6 +47,7 @@ def test_config3_forward_and_gfd_on_the_1m_face_torus(gpu, ref):
     g = 2.0 * (m.embed(fwd.face, fwd.bary) - q)      # gradcheck.cpp:88
     theirs = rm.gfd(f, b, d, g=g)                    # gfd_batched_many, diff.cpp:273-326
     runs = {"siblings": m.gfd(f, b, d, g=g), "plain": m.gfd(f, b, d, g=g, plain_schedule=True),
+            "face order": m.gfd(f, b, d, g=g, plain_schedule=2), "face order, known base": m.gfd(f, b, d, g=g, base=fwd, plain_schedule=2),
             "known base": m.gfd(f, b, d, g=g, base=fwd,
                                 out=dict(jv=np.zeros((n, 4)), jp=np.zeros((n, 4)), degraded=np.zeros((n, 4), np.uint8),
                                          frames=np.zeros((n, gpu.capi.FRAME_DOUBLES)), grad_v=np.zeros((n, 3)),
@@ -66,6 +67,8 @@ def test_config3_forward_and_gfd_on_the_1m_face_torus(gpu, ref):
     for k in ("jv", "jp", "degraded", "grad_v", "grad_p"):   # a schedule is only a schedule
         assert np.array_equal(runs["siblings"][k], runs["plain"][k]), k
         assert np.array_equal(runs["siblings"][k], runs["known base"][k]), k
+        assert np.array_equal(runs["siblings"][k], runs["face order"][k]), k
+        assert np.array_equal(runs["siblings"][k], runs["face order, known base"][k]), k
     # random starts never take a vertex branch on this mesh, so the Jacobians are in fact bit-equal
     assert not theirs["degraded"].any()
     assert np.array_equal(runs["siblings"]["jv"], theirs["jv"]) and np.array_equal(runs["siblings"]["jp"], theirs["jp"])
