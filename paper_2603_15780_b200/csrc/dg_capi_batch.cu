@@ -207,10 +207,14 @@ static int batch_trace_streamed(dg_batch* b, int64_t n, const dg_trace_in* in, c
   };
   note(cudaMemsetAsync(b->up_word, 0, sizeof(unsigned long long), s_in));
   note(cudaEventRecord(b->ev_zero, s_in));
-  // a small first piece starts the walker early; the rest arrives in a few large pieces (the link is ~4 x faster
-  // than the walker consumes queries)
+  // Small first pieces start the walker early, the rest arrives in a few large ones (the link is ~4 x faster than
+  // the walker consumes queries): 2^15, 2^15, 2^16, 2^17, then 2^18 queries each -- the resident lanes all have work
+  // within ~0.1 ms. Every piece is queued BEFORE the walker is launched (~60 us of this thread): a launch that
+  // blocks its thread until the kernel has ended -- any launch under a profiler or a sanitizer -- must not be
+  // left waiting for queries this thread has yet to queue.
   const int64_t first = std::min<int64_t>(n, int64_t(1) << 15), piece = int64_t(1) << 18;
   upload(0, first);
+  for (int64_t lo = first; lo < n;) { const int64_t len = std::min(piece, lo); upload(lo, std::min(n, lo + len)); lo += len; }
   dg::TraceParams p = p_in;
   p.queue_head = b->ctr;
   p.total_crossings = b->ctr + 1;
@@ -226,8 +230,6 @@ static int batch_trace_streamed(dg_batch* b, int64_t n, const dg_trace_in* in, c
   b->words[1] = 0;
   note(cudaMemcpyAsync(&b->words[0], b->ctr + 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, s_walk));
   note(cudaMemcpyAsync(&b->words[1], b->chunk_done + K, sizeof(unsigned int), cudaMemcpyDeviceToHost, s_walk));
-  // pieces of 2^15, 2^15, 2^16, 2^17, then 2^18 queries: the resident lanes all have work within ~0.1 ms
-  for (int64_t lo = first; lo < n;) { const int64_t len = std::min(piece, lo); upload(lo, std::min(n, lo + len)); lo += len; }
   if (e == cudaSuccess) {
     const volatile unsigned int* flags = b->chunk_flags;
     bool walker_gone = false;

@@ -18,13 +18,13 @@ capture() {  # name, launches of trace_fast_kernel to skip, mangled-name substri
   python profiles/ncu_line_profile.py /tmp/prof/${name}_sass.csv /tmp/prof/trace_dis.txt "$mangled" > $OUT/${name}_line_profile.txt 2>&1
   rm -f /tmp/prof/$name.ncu-rep /tmp/prof/${name}_sass.csv
 }
-capture r2_c2_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0" python scripts/profile_target.py c2 forward exact
-capture r2_c2_forward_fastlane 2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi1" python scripts/profile_target.py c2 forward fast
-capture r2_c3_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0" python scripts/profile_target.py c3 forward exact
+capture r2_c2_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0ELb0E" python scripts/profile_target.py c2 forward exact
+capture r2_c2_forward_fastlane 2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi1ELb0E" python scripts/profile_target.py c2 forward fast
+capture r2_c3_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0ELb0E" python scripts/profile_target.py c3 forward exact
 # (a fused call launches the walker three times: seeds, round 2, par jobs -- the eighth launch is round 2 of call 3)
-capture r2_c3_fused_gfd        7 "trace_fast_kernelILb1ELi0ELi0ELb1ELi0" python scripts/profile_target.py c3 fused exact
-capture r2_c4_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0" python scripts/profile_target.py c4 forward exact
-capture r2_c5_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0" python scripts/profile_target.py c5 forward exact
+capture r2_c3_fused_gfd        7 "trace_fast_kernelILb1ELi0ELi0ELb1ELi0ELb0E" python scripts/profile_target.py c3 fused exact
+capture r2_c4_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0ELb0E" python scripts/profile_target.py c4 forward exact
+capture r2_c5_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0ELb0E" python scripts/profile_target.py c5 forward exact
 if [ -n "$ONLY" ]; then ls -la $OUT; exit 0; fi
 # every launch of a short default bench run with its device time (cold-cache, serialised: compare SHARES)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/r2_launches_bench.csv \
