@@ -494,6 +494,12 @@ static int batch_gfd_one(dg_batch* b, double eps_v, double eps_p, const double* 
       last_error() = b->gfd_msg;
       return b->gfd_rc;
     }
+    // the Jacobians leave on a stream of their own while g arrives and the pull-back runs (the two copy directions
+    // do not share an engine)
+    cudaStream_t sj = b->streams[1];
+    if (jv) note(cudaMemcpyAsync(jv, b->jv, N * 32, cudaMemcpyDeviceToHost, sj));
+    if (jp) note(cudaMemcpyAsync(jp, b->jp, N * 32, cudaMemcpyDeviceToHost, sj));
+    if (degraded) note(cudaMemcpyAsync(degraded, b->degraded, N * 4, cudaMemcpyDeviceToHost, sj));
     if (g) {
       note(cudaMemcpyAsync(b->g, g, N * 24, cudaMemcpyHostToDevice, st));
       dg::GfdPullback pb{};
@@ -505,10 +511,8 @@ static int batch_gfd_one(dg_batch* b, double eps_v, double eps_p, const double* 
       if (grad_v) note(cudaMemcpyAsync(grad_v, b->grad_v, N * 24, cudaMemcpyDeviceToHost, st));
       if (grad_p) note(cudaMemcpyAsync(grad_p, b->grad_p, N * 24, cudaMemcpyDeviceToHost, st));
     }
-    if (jv) note(cudaMemcpyAsync(jv, b->jv, N * 32, cudaMemcpyDeviceToHost, st));
-    if (jp) note(cudaMemcpyAsync(jp, b->jp, N * 32, cudaMemcpyDeviceToHost, st));
-    if (degraded) note(cudaMemcpyAsync(degraded, b->degraded, N * 4, cudaMemcpyDeviceToHost, st));
     note(cudaStreamSynchronize(st));
+    note(cudaStreamSynchronize(sj));
     if (e != cudaSuccess) return fail_cuda(e, "dg_batch_gfd");
     return DG_OK;
   }

@@ -95,6 +95,20 @@ def test_resident_batch_on_a_device_set(gpu):
     ba.close(); bc.close()
 
 
+def test_streamed_forward_on_a_device_set(gpu):
+    """Shards of >= 2^18 queries each run the STREAMED forward (one persistent walker per device, upload cursor and
+    completion flags of its own): two of them side by side -- here on one GPU -- give the bits of one device."""
+    one, many, f, b, d = setup(gpu, 2, n=2 * (1 << 18) + 70_001)
+    ba, bc = gpu.Batch(one, len(f)), gpu.Batch(many, len(f))
+    ra, rc = ba.trace(f, b, d), bc.trace(f, b, d)
+    for k in FIELDS:
+        assert np.array_equal(getattr(ra, k), getattr(rc, k)), k
+    assert ra.total_crossings == rc.total_crossings == int(ra.crossings.sum())
+    g = np.random.default_rng(4).normal(size=(len(f), 3))
+    assert np.array_equal(ba.ep_backward(g), bc.ep_backward(g))
+    ba.close(); bc.close()
+
+
 def test_device_mode_fans_out_through_peer_copies(gpu):
     import torch
     one, many, f, b, d = setup(gpu, 3, n=90_000)
