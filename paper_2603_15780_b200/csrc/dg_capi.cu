@@ -117,9 +117,13 @@ bool encode_record_map(const dg::HalfEdgeRec* he, size_t rows, unsigned char* ou
 // mixes them with plain edge-crossing traces executes both paths one after the other (c5, 1 M geodesics: 853 ms
 // mixed, 506 ms with the two kinds in warps of their own). A schedule only: results stay at the request index.
 __global__ void sort_keys_kernel(const int32_t* __restrict__ face, const double* __restrict__ bary, int64_t n, int32_t nf,
-                                 int bits, int32_t* keys, int32_t* index) {
+                                 int bits, int32_t* keys, int32_t* index, const double* __restrict__ dir, double* length_sum) {
   int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= n) return;
+  if (length_sum && (i & 63) == 0) {   // requested length of every 64th query (finite ones)
+    const double x = dir[3 * i], y = dir[3 * i + 1], z = dir[3 * i + 2], len = sqrt(x * x + y * y + z * z);
+    if (len < 1e300) atomicAdd(length_sum, len);
+  }
   const int32_t f = face[i];
   const double b0 = bary[3 * i], b1 = bary[3 * i + 1], b2 = bary[3 * i + 2];
   const double hi = 1.0 - 1e-10;
@@ -139,7 +143,7 @@ static bool schedules_by_face(const dg_mesh* mesh, int64_t n, const dg_trace_cfg
 // The permutation that lists n device-resident queries in start-face order (vertex starts last), in staging of
 // the call; null when the staging could not be had (the request then runs in plain order).
 const int32_t* dgapi::start_face_order(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, Stage& st,
-                                       cudaStream_t stream) {
+                                       cudaStream_t stream, const double* dir, double* length_sum) {
   const size_t N = size_t(n);
   int32_t* keys_in = st.scratch<int32_t>(N);
   int32_t* keys_out = st.scratch<int32_t>(N);
@@ -148,7 +152,8 @@ const int32_t* dgapi::start_face_order(const dg_mesh* mesh, int64_t n, const int
   if (!keys_in || !keys_out || !iota || !perm) return nullptr;
   int bits = 1;
   while ((int64_t(1) << bits) < int64_t(mesh->nf) && bits < 30) ++bits;
-  sort_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(face, bary, n, mesh->nf, bits, keys_in, iota);
+  sort_keys_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(face, bary, n, mesh->nf, bits, keys_in, iota, dir,
+                                                                  dir ? length_sum : nullptr);
   size_t tmp_bytes = 0;
   st.note(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, iota, perm, int(n), 0, bits + 1, stream));
   void* tmp = st.scratch<char>(tmp_bytes);
@@ -382,6 +387,16 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   m->device = g_device;
   m->nf = nf;
   m->nv = nv;
+  {   // mean length of a face's edges: the length scale of the schedule's estimate of a trace's crossings
+    double sum = 0.0;
+    for (int32_t f = 0; f < nf; ++f)
+      for (int k = 0; k < 3; ++k) {
+        const double* a = xyz + 3 * size_t(tri[3 * size_t(f) + size_t(k)]);
+        const double* b = xyz + 3 * size_t(tri[3 * size_t(f) + size_t((k + 1) % 3)]);
+        sum += std::sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]) + (a[2] - b[2]) * (a[2] - b[2]));
+      }
+    m->mean_edge = sum / (3.0 * double(nf));
+  }
   auto cleanup = [&](int rc) { dg_mesh_destroy(m); return rc; };
   cudaError_t e;
 #define DG_TRY(expr) if ((e = (expr)) != cudaSuccess) return cleanup(fail_cuda(e, #expr))
@@ -708,11 +723,11 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   p.lane_fast = c.lane == DG_LANE_FAST;
 
   // the work cursor and the crossing total of THIS call, stream-ordered like the rest of its staging
-  unsigned long long* ctr = st.scratch<unsigned long long>(2);
+  unsigned long long* ctr = st.scratch<unsigned long long>(3);   // [2]: sum of sampled requested lengths (a double)
   if (!ctr) return fail_cuda(st.error(), "dg_trace_batch staging");
   p.queue_head = ctr;
   p.total_crossings = total_dst ? ctr + 1 : nullptr;
-  st.note(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), stream));
+  st.note(cudaMemsetAsync(ctr, 0, 3 * sizeof(unsigned long long), stream));
 
   // Schedule in start-face order (results stay at the request index). AUTO: on for large batches on meshes whose
   // crossing records do not fit the L2 -- traces that start side by side walk through the same neighbourhood at the
@@ -721,13 +736,39 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   // c2, L2-resident: +-1 %, stays off). The face order of the mesh is the caller's: a locality-preserving
   // numbering (grid, Morton, Hilbert) is what makes neighbours in the queue neighbours on the surface.
   const bool sort = schedules_by_face(mesh, n, c, record);
-  if (sort) p.perm = start_face_order(mesh, n, p.face, p.bary, st, stream);
+  double* length_sum = reinterpret_cast<double*>(ctr + 2);
+  if (sort) p.perm = start_face_order(mesh, n, p.face, p.bary, st, stream, p.dir, length_sum);
   if (st.error() != cudaSuccess) return fail_cuda(st.error(), "dg_trace_batch staging");
 
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || record ||
                           out->payload || out->transport;
   dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm), int(c.walker)};
-  st.note(dg::launch_trace(p, c.use_f32 != 0, needs_full, shape, stream));
+  // Start-face order keeps the per-lane loads ahead only while the traces that start side by side STAY side by
+  // side. Long traces spread over the mesh, the wavefront outgrows the L2 and every lane's four sector requests
+  // go to HBM on their own: 1 M-face torus, 500 k traces in start-face order, per-lane loads against cooperative
+  // loads -- 0.75 x diameter 8.7 / 9.4 ms, 1 x 12.5 / 12.3, 1.5 x 32.3 / 18.4, 5 x 122 / 63 (config 5's random
+  // half). The requested lengths live on the device, so the choice is made there: the sort's key pass sums the
+  // length of every 64th query, both instantiations are queued with complementary gates on that sum, and the one
+  // whose side of the limit it falls on runs (the other returns at once, a few microseconds). The limit: an
+  // expected 1.15 sqrt(F) crossings per trace (about 2.2 crossings per mean edge length travelled).
+  const bool gather_by_length = sort && p.perm && !needs_full && !c.use_f32 && c.walker == DG_WALKER_AUTO && !p.lane_fast &&
+                                mesh->mean_edge > 0.0 && dg::fast_walker_gather_mode(mesh->view(), mesh->he_map_ok, false) == 2 &&
+                                dg::fast_walker_gather_mode(mesh->view(), mesh->he_map_ok, true) == 0 && !getenv("DG_FAST_GATHER");
+  if (gather_by_length) {
+    const double samples = double((n + 63) / 64);
+    p.gate = length_sum;
+    p.gate_limit = samples * 1.15 * std::sqrt(double(mesh->nf)) * mesh->mean_edge / 2.2;
+    dg::TraceParams q = p;
+    p.gate_above = 0;
+    q.gate_above = 1;
+    dg::LaunchShape loads = shape, coop = shape;
+    loads.walker = DG_WALKER_FAST_LOADS;
+    coop.walker = DG_WALKER_FAST_COOP;
+    st.note(dg::launch_trace(p, false, false, loads, stream));
+    st.note(dg::launch_trace(q, false, false, coop, stream));
+  } else {
+    st.note(dg::launch_trace(p, c.use_f32 != 0, needs_full, shape, stream));
+  }
   if (total_dst) {
     st.note(cudaMemcpyAsync(total_dst, ctr + 1, sizeof(uint64_t),
                             device_mode ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));

@@ -34,6 +34,7 @@ struct dg_mesh {
   int32_t* csr_list = nullptr;
   uint8_t* vboundary = nullptr;
   int64_t bytes = 0;
+  double mean_edge = 0.0;   // mean length of a face's edges (the length scale of the schedule's trace-length estimate)
   cudaStream_t stream = nullptr;
   // small-batch path: one pinned host block + one device block, reused across calls
   mutable std::mutex small_mu;
@@ -258,8 +259,10 @@ class PeerStage {
 // Start-face scheduling (dg_capi.cu): whether the mesh's crossing records exceed what the L2 holds, and the
 // permutation that lists n device-resident queries in start-face order (null: staging failed, run in plain order).
 bool beyond_l2(const dg_mesh* mesh);
+// length_sum (optional, device, zeroed by the caller): receives the sum of the requested lengths |dir| of every
+// 64th query -- what decides the gather of a long-trace batch (enqueue_trace).
 const int32_t* start_face_order(const dg_mesh* mesh, int64_t n, const int32_t* face, const double* bary, Stage& st,
-                                cudaStream_t stream);
+                                cudaStream_t stream, const double* dir = nullptr, double* length_sum = nullptr);
 
 void poly_store_free(dg_poly_store* s);
 // Builds the half-size records of the tolerance lane on first use (no-op afterwards; quietly leaves he64 null when

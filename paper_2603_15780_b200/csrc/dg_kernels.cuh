@@ -63,6 +63,12 @@ struct TraceParams {
   uint8_t want_q;
   uint8_t he_map_ok;  // he_map is a valid tensor map of mesh.he
   uint8_t lane_fast;  // DG_LANE_FAST: plain forward requests over crossing records run the tolerance lane
+  // Gate: the launch runs only if (*gate > gate_limit) == (gate_above != 0); null = runs. Two launches of one
+  // request with complementary gates let a statistic computed on the device choose between two instantiations
+  // without a host round trip (the gather of a batch in start-face order, dg_capi.cu).
+  const double* gate;
+  double gate_limit;
+  uint8_t gate_above;
   // Streamed request (launch_trace_streamed; plain order only): the queries arrive and the results leave WHILE the
   // walker runs. The copy stream that uploads the queries chunk by chunk advances *stream_uploaded behind every
   // chunk; a warp takes work only below it. Every finished trace counts into its chunk (1 << stream_shift

@@ -192,3 +192,23 @@ def test_config3_strong_scaling_shards_give_the_bits_of_the_whole(gpu):
             part = m.trace_batch(f[sl], b[sl], d[sl])
             for k in ("face", "bary", "dir", "traced", "term"):
                 assert np.array_equal(getattr(part, k), getattr(whole, k)[sl]), (world, r, k)
+
+
+def test_gather_of_a_batch_in_start_face_order_follows_the_trace_length(gpu):
+    """On a mesh beyond the L2 a batch in start-face order is queued on both gathers with complementary gates on the
+    mean requested length (summed on the device): short traces run the per-lane loads, long ones the cooperative
+    gather. Whatever runs, exactly one of the two does, and the bits are those of either gather on its own."""
+    from paper_2603_15780_b200 import workloads as W
+    xyz, tri = W.torus(1 / 3, 1 / 6, 1000, 500)
+    m = gpu.Mesh(xyz, tri)
+    n = 40_000
+    for mult in (0.3, 4.0):   # x outer diameter: ~310 and ~4 200 crossings per trace, either side of 1.15 sqrt(F)
+        f, b, d = W.sample_queries(xyz, tri, n, mult * 1.0, seed=17)
+        auto = m.trace_batch(f, b, d, sort_by_face=True)
+        assert auto.total_crossings == int(auto.crossings.sum()) and (auto.status == 0).all()
+        assert abs(auto.traced - auto.requested).max() <= 1e-9
+        for walker in ("loads", "coop"):
+            one = m.trace_batch(f, b, d, sort_by_face=True, walker=walker)
+            for k in ("face", "bary", "dir", "traced", "term", "status", "crossings"):
+                assert np.array_equal(getattr(auto, k), getattr(one, k)), (mult, walker, k)
+            assert one.total_crossings == auto.total_crossings
