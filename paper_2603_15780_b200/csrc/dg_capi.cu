@@ -751,7 +751,7 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   // length of every 64th query, both instantiations are queued with complementary gates on that sum, and the one
   // whose side of the limit it falls on runs (the other returns at once, a few microseconds). The limit: an
   // expected 1.15 sqrt(F) crossings per trace (about 2.2 crossings per mean edge length travelled).
-  const bool gather_by_length = sort && p.perm && !needs_full && !c.use_f32 && c.walker == DG_WALKER_AUTO && !p.lane_fast &&
+  const bool gather_by_length = sort && p.perm && !needs_full && !c.use_f32 && c.walker == DG_WALKER_AUTO &&
                                 mesh->mean_edge > 0.0 && dg::fast_walker_gather_mode(mesh->view(), mesh->he_map_ok, false) == 2 &&
                                 dg::fast_walker_gather_mode(mesh->view(), mesh->he_map_ok, true) == 0 && !getenv("DG_FAST_GATHER");
   if (gather_by_length) {
@@ -761,6 +761,8 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
     dg::TraceParams q = p;
     p.gate_above = 0;
     q.gate_above = 1;
+    q.mesh.he64 = nullptr;   // (the tolerance lane has no cooperative gather of its half-size records: long traces
+                             // run its instantiation over the 128-byte records)
     dg::LaunchShape loads = shape, coop = shape;
     loads.walker = DG_WALKER_FAST_LOADS;
     coop.walker = DG_WALKER_FAST_COOP;

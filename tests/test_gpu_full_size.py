@@ -212,3 +212,7 @@ def test_gather_of_a_batch_in_start_face_order_follows_the_trace_length(gpu):
             for k in ("face", "bary", "dir", "traced", "term", "status", "crossings"):
                 assert np.array_equal(getattr(auto, k), getattr(one, k)), (mult, walker, k)
             assert one.total_crossings == auto.total_crossings
+        # the tolerance lane takes the same two roads (half-size records / 128-byte records with the cooperative gather)
+        fast = m.trace_batch(f, b, d, sort_by_face=True, lane="fast")
+        assert np.array_equal(fast.face, auto.face) and np.array_equal(fast.crossings, auto.crossings)
+        assert np.abs(m.embed(fast.face, fast.bary) - m.embed(auto.face, auto.bary)).max() <= 1e-9 * 1.1
