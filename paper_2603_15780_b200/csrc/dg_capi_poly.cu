@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(1024) poly_scan_compact_small_kernel(const int
                                                                        int32_t cap, const int32_t* __restrict__ s_face,
                                                                        const double* __restrict__ s_bary,
                                                                        const double* __restrict__ s_seg, char* packed,
-                                                                       unsigned long long* overflow) {
+                                                                       unsigned long long* overflow,
+                                                                       unsigned long long* words_out) {
   __shared__ int64_t part[1024];
   const int t = threadIdx.x;
   const int per = (n + 1023) / 1024, lo = min(n, t * per), hi = min(n, lo + per);
@@ -88,6 +89,10 @@ __global__ void __launch_bounds__(1024) poly_scan_compact_small_kernel(const int
     const int64_t src = int64_t(q) * cap, dst = offsets[q];
     for (int32_t j = lane; j < np; j += 32) { c_face[dst + j] = s_face[src + j]; c_seg[dst + j] = s_seg[src + j]; }
     for (int32_t j = lane; j < 3 * np; j += 32) c_bary[3 * dst + j] = s_bary[3 * src + j];
+  }
+  if (words_out) {   // mapped call: the work counters {queue head, total crossings, overflow count} go to the host block too
+    __syncthreads();
+    if (t == 0) { words_out[0] = overflow[-2]; words_out[1] = overflow[-1]; words_out[2] = overflow[0]; }
   }
 }
 
@@ -163,7 +168,8 @@ static int trace_polylines_small(const dg_mesh* mesh, int64_t n, const dg_trace_
   // The smallest batches skip every copy (as dg_trace_batch does up to 256 queries): the pinned blocks are mapped
   // into the device's address space, the walker reads its queries from and writes its results to the host block,
   // the scan + compaction block writes the offsets and the packed polylines straight into the host arrays; only
-  // the work counters and the slots live in device memory. One memset, two launches, one synchronisation.
+  // the work counters and the slots live in device memory (the second launch hands the counters to the host block).
+  // One memset, two launches, one synchronisation.
   const bool mapped = n <= 256 && slots <= (size_t(1) << 18);
   if (mapped && ps.points_bytes < PackedPoints(slots).bytes) {
     cudaFreeHost(ps.points); ps.points = nullptr; ps.points_bytes = 0;
@@ -205,9 +211,10 @@ static int trace_polylines_small(const dg_mesh* mesh, int64_t n, const dg_trace_
   p.want_q = c.want_transport_matrix;
   DG_CUDA(dg::launch_trace(p, c.use_f32 != 0, true, dg::LaunchShape{mesh->sm_count, int(c.blocks_per_sm), int(c.walker)}, stream));
   poly_scan_compact_small_kernel<<<1, 1024, 0, stream>>>(p.o_npoints, d_off, int(n), cap, p.poly_face, p.poly_bary, p.poly_seg,
-                                                         mapped ? ps.points : dp + packed_off, ctr + 2);
+                                                         mapped ? ps.points : dp + packed_off, ctr + 2,
+                                                         mapped ? reinterpret_cast<unsigned long long*>(hp) : nullptr);
   DG_CUDA(cudaGetLastError());
-  DG_CUDA(cudaMemcpyAsync(hp, dp, 32, cudaMemcpyDeviceToHost, stream));
+  if (!mapped) DG_CUDA(cudaMemcpyAsync(hp, dp, 32, cudaMemcpyDeviceToHost, stream));
   if (!mapped) DG_CUDA(cudaMemcpyAsync(hp + out_begin, dp + out_begin, io_bytes - out_begin, cudaMemcpyDeviceToHost, stream));
   DG_CUDA(cudaStreamSynchronize(stream));
   const int64_t* h_off = reinterpret_cast<const int64_t*>(hp + fout[12].off);
