@@ -28,6 +28,30 @@ def prefix_and_sample(n, k_prefix, k_random, seed):
     return np.concatenate([np.arange(k_prefix), np.sort(rng.choice(np.arange(k_prefix, n), k_random, replace=False))])
 
 
+def test_config2_training_step_through_host_buffers_at_full_size(gpu, ref):
+    """The headline path of bench.py's `e2e`: config 2's 1 M geodesics through the resident batch on host buffers --
+    the STREAMED forward (one walker while queries arrive and results leave), then EP on the resident samples --
+    against the reference on a prefix + random sample taken out of the full-batch run: every bit."""
+    from bench import make_workload
+    n = 1_000_000
+    xyz, tri, f, b, d, q = make_workload("c2", n, 42)
+    m = gpu.Mesh(xyz, tri)
+    rm = ref.RefMesh.build(xyz, tri)
+    batch = gpu.Batch(m, n)
+    h = batch.trace(f, b, d)
+    g = 2.0 * (m.embed(h.face, h.bary) - q)          # gradcheck.cpp:88
+    gv = batch.ep_backward(g)
+    assert h.total_crossings == int(h.crossings.sum()) and (h.status == 0).all() and (h.term == 0).all()
+    sel = prefix_and_sample(n, 6000, 6000, 2)
+    r = rm.trace_batch(f[sel], b[sel], d[sel], record_polyline=True)
+    for k in ("face", "bary", "dir", "traced", "term", "status"):
+        assert np.array_equal(getattr(r, k), getattr(h, k)[sel]), k
+    assert np.array_equal(r.npoints - 2, h.crossings[sel])       # one polyline point per crossing + start + end
+    theirs = rm.ep(f[sel], b[sel], d[sel], r.face, r.bary, r.dir, g=g[sel])
+    assert np.array_equal(theirs["grad_v"], gv[sel])
+    batch.close()
+
+
 def test_config3_forward_and_gfd_on_the_1m_face_torus(gpu, ref):
     """Config 3: 1 M-face noisy torus, bench stream (seed 42), forward + GFD with the default eps.
     6 000-sample prefix: jv / jp <= 1e-5 relative, degraded flags and frames bit-equal, pulled-back
