@@ -365,7 +365,10 @@ DG_API int dg_batch_create(const dg_mesh* mesh, int64_t capacity, dg_batch** out
 DG_API void dg_batch_destroy(dg_batch* b);
 DG_API int64_t dg_batch_size(const dg_batch* b);
 /* Plain forward exp map (no payload / transport matrix / hole avoidance / polylines: those go
- * through dg_trace_batch). cfg->memory must be DG_MEM_HOST and cfg->stream NULL. */
+ * through dg_trace_batch). cfg->memory must be DG_MEM_HOST and cfg->stream NULL. From 2^18 queries in plain order
+ * the call is streamed: one persistent walker runs while the queries arrive and the results leave, and the calling
+ * thread spins on per-chunk completion flags to queue the copies back; below that, or in start-face
+ * order, slices on separate streams. Same bits either way. */
 DG_API int dg_batch_trace(dg_batch* b, int64_t n, const dg_trace_in* in, const dg_trace_cfg* cfg,
                           dg_trace_out* out);
 /* The forward of a step whose backward will be GFD: dg_trace_gfd on the resident batch (forward results out, the
