@@ -582,7 +582,7 @@ def measure(key, args, ctx, headline):
         if face_order and mesh.gather == "coop":
             # on meshes beyond 250 MB of records a batch in start-face order is queued on both gathers and the mean
             # requested length, summed on the device, decides which one runs
-            gather_kind = "loads while the traces are short (an expected < 1.15 sqrt(F) crossings), else coop: decided on the device"
+            gather_kind = "loads while the wavefront stays near the L2 (expected crossings x sqrt(F) < 1e6), else coop: decided on the device"
         gather = {"gather": gather_kind, "start_face_order": face_order, "record_bytes": 3 * mesh.nf * 128, "achieved_grecords_per_s": cps_fwd / 1e9,
                   "peak_grecords_per_s": peak_g, "frac": cps_fwd / 1e9 / peak_g, "random_gather_grecords_per_s": gather_rates,
                   "source": "scripts/micro/gather_bench run inside this bench before the timed region; peak = the best of its "

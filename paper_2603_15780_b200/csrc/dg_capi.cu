@@ -743,29 +743,33 @@ static int enqueue_trace(const dg_mesh* mesh, int64_t n, const dg_trace_in* in, 
   const bool needs_full = in->payload || c.want_transport_matrix || c.hole_avoidance || record ||
                           out->payload || out->transport;
   dg::LaunchShape shape{mesh->sm_count, int(c.blocks_per_sm), int(c.walker)};
-  // Start-face order keeps the per-lane loads ahead only while the traces that start side by side STAY side by
-  // side. Long traces spread over the mesh, the wavefront outgrows the L2 and every lane's four sector requests
-  // go to HBM on their own: 1 M-face torus, 500 k traces in start-face order, per-lane loads against cooperative
-  // loads -- 0.75 x diameter 8.7 / 9.4 ms, 1 x 12.5 / 12.3, 1.5 x 32.3 / 18.4, 5 x 122 / 63 (config 5's random
-  // half). The requested lengths live on the device, so the choice is made there: the sort's key pass sums the
-  // length of every 64th query, both instantiations are queued with complementary gates on that sum, and the one
-  // whose side of the limit it falls on runs (the other returns at once, a few microseconds). The limit: an
-  // expected 1.15 sqrt(F) crossings per trace (about 2.2 crossings per mean edge length travelled).
-  const bool gather_by_length = sort && p.perm && !needs_full && !c.use_f32 && c.walker == DG_WALKER_AUTO &&
-                                mesh->mean_edge > 0.0 && dg::fast_walker_gather_mode(mesh->view(), mesh->he_map_ok, false) == 2 &&
-                                dg::fast_walker_gather_mode(mesh->view(), mesh->he_map_ok, true) == 0 && !getenv("DG_FAST_GATHER");
-  if (gather_by_length) {
-    const double samples = double((n + 63) / 64);
-    p.gate = length_sum;
-    p.gate_limit = samples * 1.15 * std::sqrt(double(mesh->nf)) * mesh->mean_edge / 2.2;
-    dg::TraceParams q = p;
-    p.gate_above = 0;
-    q.gate_above = 1;
-    q.mesh.he64 = nullptr;   // (the tolerance lane has no cooperative gather of its half-size records: long traces
-                             // run its instantiation over the 128-byte records)
+  // Start-face order keeps the per-lane loads ahead only while the records the resident lanes walk over stay within
+  // reach of the L2; beyond that every lane's four sector requests go to HBM on their own and the cooperative gather
+  // (one line request per record) is 1.5-2.8 x faster. Consecutive entries of the order start in a band across the
+  // mesh, and a trace of L crossings carries the band L / 2 cells further: the footprint of the wavefront grows as
+  // L sqrt(F) faces, whatever the size of the batch. Measured on tori of 1 M / 2.25 M / 4 M faces with 0.5 M - 10 M
+  // traces (scripts/dev/gather_crossover.py, per-lane / cooperative, ms): 1 M faces, 500 k traces of 520 crossings
+  // 5.9 / 6.3, 1 045 crossings 12.5 / 12.4, 1 570 32.3 / 18.4, 5 220 (config 5's random half) 122 / 62; 2.25 M faces,
+  // 4 M traces of 510 crossings 42.5 / 47.4, 1 020 203 / 92; 4 M faces, 10 M traces of 680 crossings 312 / 162 -- the
+  // two tie at L sqrt(F) = 1e6 in every case. L is known only on the device (the requested lengths), so the sort's
+  // key pass sums the length of every 64th query, both instantiations are queued with complementary gates on that
+  // sum, and the one whose side of the limit it falls on runs (the other returns at once): no host round trip, the
+  // call stays asynchronous. (About 2.5 crossings per mean edge length travelled.)
+  const bool two_gathers = sort && p.perm && !needs_full && !c.use_f32 && c.walker == DG_WALKER_AUTO && mesh->mean_edge > 0.0 &&
+                           dg::fast_walker_gather_mode(mesh->view(), mesh->he_map_ok, false) == 2 &&
+                           dg::fast_walker_gather_mode(mesh->view(), mesh->he_map_ok, true) == 0 && !getenv("DG_FAST_GATHER");
+  if (two_gathers) {
     dg::LaunchShape loads = shape, coop = shape;
     loads.walker = DG_WALKER_FAST_LOADS;
     coop.walker = DG_WALKER_FAST_COOP;
+    dg::TraceParams q = p;
+    q.mesh.he64 = nullptr;   // (the tolerance lane has no cooperative gather of its half-size records: its
+                             // instantiation over the 128-byte records takes that road)
+    const double samples = double((n + 63) / 64), tie_crossings = 1e6 / std::sqrt(double(mesh->nf));
+    p.gate = q.gate = length_sum;
+    p.gate_limit = q.gate_limit = samples * tie_crossings * mesh->mean_edge / 2.5;
+    p.gate_above = 0;
+    q.gate_above = 1;
     st.note(dg::launch_trace(p, false, false, loads, stream));
     st.note(dg::launch_trace(q, false, false, coop, stream));
   } else {

@@ -226,7 +226,7 @@ def test_gather_of_a_batch_in_start_face_order_follows_the_trace_length(gpu):
     xyz, tri = W.torus(1 / 3, 1 / 6, 1000, 500)
     m = gpu.Mesh(xyz, tri)
     n = 40_000
-    for mult in (0.3, 4.0):   # x outer diameter: ~310 and ~4 200 crossings per trace, either side of 1.15 sqrt(F)
+    for mult in (0.3, 4.0):   # x outer diameter: ~310 and ~4 200 crossings per trace, either side of 1e6 / sqrt(F)
         f, b, d = W.sample_queries(xyz, tri, n, mult * 1.0, seed=17)
         auto = m.trace_batch(f, b, d, sort_by_face=True)
         assert auto.total_crossings == int(auto.crossings.sum()) and (auto.status == 0).all()
