@@ -224,8 +224,11 @@ typedef struct dg_trace_out {
 DG_API int dg_trace_batch(const dg_mesh* mesh, int64_t n, const dg_trace_in* in,
                           const dg_trace_cfg* cfg, dg_trace_out* out);
 /* What a plain f64 forward request of n queries gets under cfg (NULL = defaults): *face_order = 1 when it is
- * scheduled in start-face order (dg_trace_cfg.sort_by_face resolved), *gather = the DG_GATHER_* of its launch
- * (start-face order keeps the per-lane loads at every mesh size). For reports; same bits whatever the plan. */
+ * scheduled in start-face order (dg_trace_cfg.sort_by_face resolved), *gather = the DG_GATHER_* of its launch.
+ * Under start-face order that is the per-lane loads; on a mesh beyond 250 MB of records the request is queued on
+ * the cooperative gather as well and the requested lengths, summed on the device, decide which of the two runs
+ * (long traces: expected crossings x sqrt(faces) > 1e6 -- the cooperative one). For reports; same bits whatever
+ * the plan. */
 DG_API int dg_trace_plan(const dg_mesh* m, int64_t n, const dg_trace_cfg* cfg, int* face_order, int* gather);
 
 /* trace_batch with the reference's DEFAULT TraceConfig, record_polyline = true (tracer.hpp:22), in ONE call: the
