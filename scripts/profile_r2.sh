@@ -24,7 +24,10 @@ capture r2_c3_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0ELb0E" py
 # (a fused call launches the walker three times: seeds, round 2, par jobs -- the eighth launch is round 2 of call 3)
 capture r2_c3_fused_gfd        7 "trace_fast_kernelILb1ELi0ELi0ELb1ELi0ELb0E" python scripts/profile_target.py c3 fused exact
 capture r2_c4_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0ELb0E" python scripts/profile_target.py c4 forward exact
-capture r2_c5_forward          2 "trace_fast_kernelILb1ELi0ELi0ELb0ELi0ELb0E" python scripts/profile_target.py c5 forward exact
+# (a batch in start-face order on a mesh beyond 250 MB of records is queued on both gathers, one of which returns at
+# once: c3 / c4 run the per-lane loads -- the third launch is call 2's --, config 5's long traces the cooperative
+# gather: the sixth launch is call 3's)
+capture r2_c5_forward          5 "trace_fast_kernelILb1ELi2ELi0ELb0ELi0ELb0E" python scripts/profile_target.py c5 forward exact
 if [ -n "$ONLY" ]; then ls -la $OUT; exit 0; fi
 # every launch of a short default bench run with its device time (cold-cache, serialised: compare SHARES)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/r2_launches_bench.csv \
