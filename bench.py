@@ -401,6 +401,8 @@ def measure(key, args, ctx, headline):
             mesh.gfd_pullback_device(F, D, o["face"], blk.col["jv"], blk.col["jp"], G, blk.col["grad_v"], blk.col["grad_p"])
             launches = 2 + 2 + 3 + 1   # round 1 (job builder, seeds walker), round 2 (job builder, 4-sibling walker),
             #                            par jobs (builder, walker), assemble; pull-back
+            if face_order:
+                launches += 1          # the key pass of the sample order (the radix sort itself is cub's)
             if world > 1:
                 gather()
             if timed:
@@ -410,6 +412,8 @@ def measure(key, args, ctx, headline):
         mesh.trace_batch_device(F, B, D, o, max_steps=max_steps)
         e1.record()
         launches = 1
+        if face_order:                 # the key pass of the start-face order (the radix sort itself is cub's) and, on a
+            launches += 2 if mesh.gather == "coop" else 1   # mesh beyond 250 MB, the second launch of the gated pair
         if scheme == "ep":
             mesh.ep_backward_device(F, D, o["face"], o["dir"], G, blk.col["grad_v"], blk.col["grad_p"])
             launches += 1
