@@ -179,6 +179,13 @@ def test_streamed_forward_gives_the_bits_of_the_sliced_pipeline(gpu, ref, monkey
     gv = batch.ep_backward(g)
     sep = m.ep_backward(f2[:5000], d2[:5000], h2.face[:5000], h2.dir[:5000], g[:5000])
     assert np.array_equal(gv[:5000], sep)
+    # EP on the streamed batch reports a degenerate direction with its request index (diff.cpp:46)
+    d3 = d2.copy()
+    d3[200_000] = 0.0
+    batch.trace(f2, b2, d3)
+    with pytest.raises(gpu.DgError) as err:
+        batch.ep_backward(g)
+    assert err.value.klass == "DegenerateDirection" and err.value.index == 200_000
     # the host-mode dg_trace_batch of a large plain request runs on the same pipeline
     t = m.trace_batch(f, b, d)
     assert np.array_equal(t.bary, h.bary) and np.array_equal(t.face, h.face)
