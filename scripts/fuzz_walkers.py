@@ -79,6 +79,16 @@ def main(rounds=40, n=40000, seed=0):
                     if not np.array_equal(x, y, equal_nan=True):
                         bad += 1
                         print(f"round {r} cache={m.has_transport_cache} walker={walker} scale={scale:g}: full-variant {key} differs", flush=True)
+            # the polyline-only lane (kPay = 3): the reference's default call -- polylines, no payload --, and hole
+            # avoidance without a payload
+            kw = dict(max_steps=max_steps, hole_avoidance=bool((r >> 1) % 2), record_polyline=bool(r % 2 == 0) or not (r >> 1) % 2)
+            slow_p = m.trace_batch(f, b, d, walker="generic", **kw)
+            for walker in (("loads", "tma", "coop") if m.has_transport_cache else ("auto",)):
+                fast_p = m.trace_batch(f, b, d, walker=walker, **kw)
+                for key in FIELDS + (("poly_face", "poly_bary", "poly_seg") if kw["record_polyline"] else ()):
+                    if not np.array_equal(getattr(fast_p, key), getattr(slow_p, key), equal_nan=True):
+                        bad += 1
+                        print(f"round {r} cache={m.has_transport_cache} walker={walker} scale={scale:g}: polyline-only variant {key} differs", flush=True)
             # the transport-matrix lane (kPay = 2), with and without a payload, with and without polylines
             kw = dict(max_steps=max_steps, want_q=True, hole_avoidance=bool((r >> 1) % 2), record_polyline=bool(r % 3 == 0))
             if r % 2:
