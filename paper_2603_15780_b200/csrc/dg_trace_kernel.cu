@@ -219,7 +219,9 @@ int gather_mode(const MeshView& m, int siblings, bool map_ok, int walker, bool f
   else if (walker == 4) mode = 2;
   else if (forced >= 0) mode = forced;
   // (start-face order: neighbouring lanes walk through the same neighbourhood, most sectors are L2 hits and the
-  // per-lane loads keep their lead -- c3 15.7 ms against 17.2 cooperative, c4 18.5 against 19.7)
+  // per-lane loads lead -- c3 15.7 ms against 17.2 cooperative, c4 18.5 against 19.7 -- while the traces are short
+  // for the mesh; the request layer queues long-trace batches on the cooperative gather as well and lets the
+  // requested lengths, summed on the device, pick: enqueue_trace, dg_capi.cu)
   else mode = (siblings <= 1 && !face_order && size_t(m.nf) * 3 * sizeof(HalfEdgeRec) > (size_t(250) << 20)) ? 2 : 0;
   if (mode == 1 && !map_ok) mode = 2;
   return mode;
