@@ -76,7 +76,13 @@ __device__ void store_frames(double* frames, int64_t i, const TangentFrame* fv, 
 // ------------------------------------------------------------------------------------- EP
 
 // error word: (sample << 2) | kind, kind 0 = |v| too small, 1 = normal to the face, 2 = bad face
-__global__ void __launch_bounds__(128) ep_kernel(const __grid_constant__ EpParams p) {
+// A latency-bound gather (two face records and two normals per sample, 17 % of the issue slots busy): more
+// resident warps pay -- 1 M samples, device-resident, L2 flushed: 4 blocks per SM (112 registers) 0.108 ms,
+// 5 (96 registers, 40 bytes of spill) 0.095, 6 / 8 (80 / 64 registers) 0.093 / 0.094.
+#ifndef DG_EP_MIN_BLOCKS
+#define DG_EP_MIN_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(128, DG_EP_MIN_BLOCKS) ep_kernel(const __grid_constant__ EpParams p) {
   const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (i >= p.n) return;
   const int f = p.face[i], fe = p.end_face[i];
