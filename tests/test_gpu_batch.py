@@ -179,6 +179,12 @@ def test_streamed_forward_gives_the_bits_of_the_sliced_pipeline(gpu, ref, monkey
     gv = batch.ep_backward(g)
     sep = m.ep_backward(f2[:5000], d2[:5000], h2.face[:5000], h2.dir[:5000], g[:5000])
     assert np.array_equal(gv[:5000], sep)
+    # a request of exactly 2^18 queries: whole chunks, whole pieces, the smallest streamed call
+    m18 = 1 << 18
+    e = batch.trace(f2[:m18], b2[:m18], d2[:m18])
+    for k in ("face", "bary", "dir", "traced", "crossings"):
+        assert np.array_equal(getattr(e, k), getattr(h2, k)[:m18]), k
+    assert e.total_crossings == int(h2.crossings[:m18].sum())
     # EP on the streamed batch reports a degenerate direction with its request index (diff.cpp:46)
     d3 = d2.copy()
     d3[200_000] = 0.0
