@@ -79,6 +79,17 @@ __global__ void build_halfedges_kernel(const dg::MeshView m, dg::HalfEdgeRec* he
   he[s] = r;
 }
 
+// Interior angle of every face corner, through the function the fan walk calls per fan face (dg_tracer_core.cuh).
+__global__ void build_corner_angles_kernel(const dg::MeshView m, double* cangle) {
+  using namespace dg;
+  const int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (s >= 3 * int64_t(m.nf)) return;
+  const int f = int(s / 3), k = int(s % 3);
+  const Face<double> c = load_face<double>(m, f);
+  const V3<double> x0 = c.pos(k);
+  cangle[s] = angle_between(c.pos(k == 2 ? 0 : k + 1) - x0, c.pos(k == 0 ? 2 : k - 1) - x0);
+}
+
 __global__ void build_halfedges64_kernel(const dg::MeshView m, dg::HalfEdgeRec64* he) {
   const int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (s >= 3 * int64_t(m.nf)) return;
@@ -405,11 +416,12 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   const size_t F = size_t(nf), Vn = size_t(nv);
   DG_TRY(cudaMalloc(&m->rec, F * sizeof(dg::FaceRec)));
   DG_TRY(cudaMalloc(&m->fnormal, 3 * F * sizeof(double)));
+  DG_TRY(cudaMalloc(&m->cangle, 3 * F * sizeof(double)));
   DG_TRY(cudaMalloc(&m->vangle, Vn * sizeof(double)));
   DG_TRY(cudaMalloc(&m->csr_off, (Vn + 1) * sizeof(int32_t)));
   DG_TRY(cudaMalloc(&m->csr_list, 3 * F * sizeof(int32_t)));
   DG_TRY(cudaMalloc(&m->vboundary, Vn));
-  m->bytes = int64_t(F * sizeof(dg::FaceRec) + 3 * F * 8 + Vn * 8 + (Vn + 1) * 4 + 3 * F * 4 + Vn);
+  m->bytes = int64_t(F * sizeof(dg::FaceRec) + 3 * F * 8 + 3 * F * 8 + Vn * 8 + (Vn + 1) * 4 + 3 * F * 4 + Vn);
   // Transport cache policy (384 B per face on top of the 96 B face record).
   bool cache = (flags & 3u) == DG_MESH_TRANSPORT_ON;
   if ((flags & 3u) == DG_MESH_TRANSPORT_AUTO) {
@@ -441,6 +453,10 @@ int dg_mesh_create_ex(const double* xyz, int32_t nv, const int32_t* tri, int32_t
   DG_TRY(cudaMemcpyAsync(d_tri, tri, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(cudaMemcpyAsync(d_adj, adj, 3 * F * sizeof(int32_t), cudaMemcpyHostToDevice, m->stream));
   DG_TRY(dg::launch_build_records(d_xyz, d_tri, d_adj, nf, m->rec, m->stream));
+  build_corner_angles_kernel<<<unsigned((3 * F + 127) / 128), 128, 0, m->stream>>>(m->view_uncached(), m->cangle);
+  DG_TRY(cudaGetLastError());
+  if (const char* env = getenv("DG_CORNER_ANGLES"))   // =0: the fan walk computes its angles (A/B measurements; same bits)
+    if (env[0] == '0') { cudaStreamSynchronize(m->stream); cudaFree(m->cangle); m->cangle = nullptr; m->bytes -= int64_t(3 * F * 8); }
   if (m->he) {
     build_halfedges_kernel<<<unsigned((3 * F + 127) / 128), 128, 0, m->stream>>>(m->view_uncached(), m->he);
     DG_TRY(cudaGetLastError());
@@ -497,7 +513,7 @@ void dg_mesh_destroy(dg_mesh* m) {
   if (m->small_pin) cudaFreeHost(m->small_pin);
   cudaFree(m->small_dev);
   cudaFree(m->he64);
-  cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->vangle); cudaFree(m->csr_off);
+  cudaFree(m->rec); cudaFree(m->he); cudaFree(m->fnormal); cudaFree(m->cangle); cudaFree(m->vangle); cudaFree(m->csr_off);
   cudaFree(m->csr_list); cudaFree(m->vboundary);
   if (m->stream) cudaStreamDestroy(m->stream);
   delete m;

@@ -29,6 +29,7 @@ struct dg_mesh {
   alignas(64) unsigned char he_map[128] = {};  // CUtensorMap over `he` for the TMA gather (valid iff he_map_ok)
   bool he_map_ok = false;
   double* fnormal = nullptr;
+  double* cangle = nullptr;   // per-corner interior angles (dg_mesh_view.cuh), built on the device at upload
   double* vangle = nullptr;
   int32_t* csr_off = nullptr;
   int32_t* csr_list = nullptr;
@@ -62,6 +63,7 @@ struct dg_mesh {
   dg::MeshView view() const {
     dg::MeshView v{rec, he, fnormal, vangle, csr_off, csr_list, vboundary, nf, nv};
     v.he64 = he64;
+    v.cangle = cangle;
     return v;
   }
   // the same mesh without the transport cache (f32 lane: its transports are float arithmetic)

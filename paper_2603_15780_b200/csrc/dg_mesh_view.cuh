@@ -72,6 +72,9 @@ struct MeshView {
   const uint8_t* vboundary;  // [nv]   (Mesh::vertex_on_boundary)
   int32_t nf, nv;
   const HalfEdgeRec64* he64 = nullptr;  // [3 nf] or null: the tolerance lane's half-size crossing records
+  // [3 nf] or null: interior angle of face f at corner k -- angle_between(x_{k+1} - x_k, x_{k+2} - x_k), computed at
+  // upload by the device function the fan walk (tracer.cpp:252-311) would call per fan face; f64 lane only
+  const double* cangle = nullptr;
 };
 
 // Register copy of one face record in the stepping scalar type S.
@@ -157,6 +160,16 @@ DG_HD HalfEdge load_halfedge(const MeshView& m, int f, int k) {
 #endif
   h.ja = c & 3; h.jc = (c >> 2) & 3; h.jt = (c >> 4) & 3;
   return h;
+}
+
+// The three corner angles of face f (MeshView::cangle must be non-null).
+DG_HD V3<double> load_corner_angles(const MeshView& m, int f) {
+  const double* p = m.cangle + 3 * size_t(f);
+#ifdef __CUDA_ARCH__
+  return {__ldg(p), __ldg(p + 1), __ldg(p + 2)};
+#else
+  return {p[0], p[1], p[2]};
+#endif
 }
 
 template <class S>

@@ -356,9 +356,16 @@ struct Tracer {
       int gn = G.neighbor_across(x0, x1);
       if (gn < 0) return false;
       Face<S> GN = load_face<S>(m, gn);
+      // the interior angle of the fan face at x0: from the table built at upload (the same function of the same
+      // corner vectors -- the cross product's sign is the only thing the order of the two changes, and the angle
+      // takes its norm), fetched beside the face record; computed here in the f32 lane and without a table
+      const bool tabled = sizeof(S) == sizeof(double) && m.cangle != nullptr;
+      V3<double> corner_angles{0.0, 0.0, 0.0};
+      if (tabled) corner_angles = load_corner_angles(m, gn);
       int x2 = GN.third(x0, x1);
       V3<S> x2p = GN.pos_of(x2);
-      alpha += angle_between(x1p - x0p, x2p - x0p);
+      if (tabled) alpha += S(get(corner_angles, GN.corner_of(x0)));
+      else alpha += angle_between(x1p - x0p, x2p - x0p);
       EdgeTransport<S> t = make_edge_transport(x0p, x1p, G.pos_of(G.third(x0, x1)), x2p);
       carried = t(carried);
       apply_transport(t);

@@ -294,3 +294,24 @@ def test_tolerance_lane_parity_gate(gpu, ref, key, n, records, monkeypatch):
         den = np.linalg.norm(pb[name], axis=1) * np.linalg.norm(rg[name], axis=1)
         ok = den > 1e-12
         assert (num[ok] / den[ok]).min() >= 0.999999, name
+
+
+def test_corner_angle_table_changes_no_bit(gpu, monkeypatch):
+    """The fan walk (tracer.cpp:252-311) takes the interior angle of every fan face from a table built at upload by
+    the function it would call itself: vertex-to-vertex walks with and without the table, every bit, both walkers."""
+    from paper_2603_15780_b200 import workloads as W
+    xyz, tri = W.torus(1 / 3, 1 / 6, 96, 48, noise=0.05, seed=3)
+    f, b, d = W.vertex_edge_queries(xyz, tri, 20_000, 3.0, seed=5, meridian=True)
+    fr, br, dr = W.sample_queries(xyz, tri, 5_000, 1.5, seed=6)
+    br[::3] = [1.0, 0.0, 0.0]                       # vertex starts in arbitrary directions
+    f, b, d = np.concatenate([f, fr]), np.concatenate([b, br]), np.concatenate([d, dr])
+    with_table = gpu.Mesh(xyz, tri)
+    monkeypatch.setenv("DG_CORNER_ANGLES", "0")
+    without = gpu.Mesh(xyz, tri)
+    monkeypatch.delenv("DG_CORNER_ANGLES")
+    assert with_table.device_bytes - without.device_bytes == 3 * len(tri) * 8
+    for kw in (dict(), dict(walker="generic"), dict(record_polyline=True)):
+        x, y = with_table.trace_batch(f, b, d, **kw), without.trace_batch(f, b, d, **kw)
+        for k in FIELDS + (("poly_face", "poly_bary", "poly_seg") if kw.get("record_polyline") else ()):
+            assert np.array_equal(getattr(x, k), getattr(y, k), equal_nan=True), (kw, k)
+        assert x.total_crossings == y.total_crossings and (x.npoints > 50).any()
