@@ -496,40 +496,39 @@ struct Tracer {
     int x0 = cur.id(k0);
     if (kFull && hole_avoidance && m.vboundary[x0]) return blue_vertex(x0, then_advance);
 
-    if (wedge_contains(cur, k0, -dir)) {  // arriving through this face
-      if (fan_walk(x0)) return Outcome::Continue;
-      last_event = kEvBoundaryStop;
-      return Outcome::Boundary;
-    }
-    if (wedge_contains(cur, k0, dir)) {
-      *then_advance = true;
-      return Outcome::Continue;
-    }
-
-    // departing into some other incident face: re-anchor with the best inward margin
-    int best_face = -1;
-    S best_margin = -dg_inf<S>();
-    const int beg = m.csr_off[x0], end = m.csr_off[x0 + 1];
-    for (int i = beg; i < end; ++i) {
-      int g = m.csr_list[i];
-      Face<S> G = load_face<S>(m, g);
-      S c1, c2;
-      wedge_coeffs(G, G.corner_of(x0), dir, &c1, &c2);
-      S mag = dg_abs(c1) + dg_abs(c2);
-      if (mag <= S(0)) continue;
-      S margin = (c2 < c1 ? c2 : c1) / mag;  // std::min(c1, c2) / mag
-      if (margin > best_margin) { best_margin = margin; best_face = g; }
-    }
-    if (best_face >= 0 && best_margin >= -Tol<S>::dir_rel()) {
-      PlaneProject<S> project{load_normal<S>(m, best_face)};
-      V3<S> proj = project(dir);
-      if (norm(proj) > S(0)) {
-        dir = normalized(proj);
-        apply_transport(project);
-        set_face(best_face);
-        bary = unit_axis<S>(cur.corner_of(x0));
+    // (one call site of fan_walk for both of the reference's -- arriving through this face, and no face to
+    // re-anchor in: the walk is inlined, and a second copy of it is a sixth of the kernel's instructions)
+    if (!wedge_contains(cur, k0, -dir)) {  // not arriving through this face
+      if (wedge_contains(cur, k0, dir)) {
         *then_advance = true;
         return Outcome::Continue;
+      }
+
+      // departing into some other incident face: re-anchor with the best inward margin
+      int best_face = -1;
+      S best_margin = -dg_inf<S>();
+      const int beg = m.csr_off[x0], end = m.csr_off[x0 + 1];
+      for (int i = beg; i < end; ++i) {
+        int g = m.csr_list[i];
+        Face<S> G = load_face<S>(m, g);
+        S c1, c2;
+        wedge_coeffs(G, G.corner_of(x0), dir, &c1, &c2);
+        S mag = dg_abs(c1) + dg_abs(c2);
+        if (mag <= S(0)) continue;
+        S margin = (c2 < c1 ? c2 : c1) / mag;  // std::min(c1, c2) / mag
+        if (margin > best_margin) { best_margin = margin; best_face = g; }
+      }
+      if (best_face >= 0 && best_margin >= -Tol<S>::dir_rel()) {
+        PlaneProject<S> project{load_normal<S>(m, best_face)};
+        V3<S> proj = project(dir);
+        if (norm(proj) > S(0)) {
+          dir = normalized(proj);
+          apply_transport(project);
+          set_face(best_face);
+          bary = unit_axis<S>(cur.corner_of(x0));
+          *then_advance = true;
+          return Outcome::Continue;
+        }
       }
     }
     if (fan_walk(x0)) return Outcome::Continue;
