@@ -383,7 +383,8 @@ struct Tracer {
     V3<S> e_far = normalized(x1p - x0p);
     V3<S> n_g = load_normal<S>(m, g);
     V3<S> e_near = near_vertex >= 0 ? normalized(near_pos - x0p) : rev;
-    S side = signed_angle(e_far, e_near, n_g) >= S(0) ? S(1) : S(-1);
+    // the reference takes the sign of signed_angle (tracer.cpp:294): only the sign is computed, the same predicate
+    S side = signed_angle_nonneg(e_far, e_near, n_g) ? S(1) : S(-1);
     V3<S> outgoing = rotate_about(e_far, n_g, side * beta);
     outgoing = normalized(outgoing - n_g * dot(outgoing, n_g));
 
