@@ -188,3 +188,12 @@ HC_API void hc_trace_batch_fast(void* h, int64_t n, const int32_t* face, const d
 // 1 / 2: plain forward requests over crossing records run the tolerance lane (dg_trace_cfg.lane = DG_LANE_FAST) over
 // the 128-byte records / over the half-size records
 HC_API void hc_set_lane_fast(int on) { g_lane_fast = on; }
+
+// signed_angle_nonneg (dg_math.cuh) for n triples (a, b, axis): out[i] = 1 when it holds.
+HC_API void hc_signed_angle_nonneg(int64_t n, const double* a, const double* b, const double* axis, uint8_t* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    const dg::V3<double> A{a[3 * i], a[3 * i + 1], a[3 * i + 2]}, B{b[3 * i], b[3 * i + 1], b[3 * i + 2]},
+        N{axis[3 * i], axis[3 * i + 1], axis[3 * i + 2]};
+    out[i] = dg::signed_angle_nonneg(A, B, N) ? 1 : 0;
+  }
+}

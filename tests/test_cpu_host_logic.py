@@ -161,3 +161,39 @@ def test_wire_formats_match_reference_json(ref):
     mine = dict(ours["traces"][1])
     assert mine.pop("transported_payload") == [1e-5, -2.5e20, 3.0]
     assert mine == stalled
+
+
+def test_side_predicate_equals_the_sign_of_the_reference_arctangent():
+    """The fan walk takes the side of its overshoot from `signed_angle(e_far, e_near, n) >= 0` (tracer.cpp:294,
+    geometry.hpp:56-58: atan2(dot(cross(a, b), n), dot(a, b))). The device code evaluates the same predicate without
+    the arctangent (signed_angle_nonneg, dg_math.cuh); here it is held against libm's atan2 on the same products:
+    signed zeros, NaN, infinities, tiny and random arguments."""
+    import ctypes as C
+    import hostcheck_api
+    lib = hostcheck_api.lib()
+    rng = np.random.default_rng(3)
+    special = [0.0, -0.0, 1.0, -1.0, 5e-324, -5e-324, 1e-300, -1e-300, np.inf, -np.inf, np.nan, 0.5, -0.5]
+    # a = (x, y, 0), b = (1, 0, 0) ... products chosen through axis-aligned vectors: a x b . n and a . b take every pair
+    A, B, N = [], [], []
+    for y in special:
+        for x in special:
+            # a = (1, 0, 0), b = (x, y, 0), n = (0, 0, 1): cross(a, b) = (0, 0, y), dot(a, b) = x (+ 0 terms)
+            A.append((1.0, 0.0, 0.0)); B.append((x, y, 0.0)); N.append((0.0, 0.0, 1.0))
+    a = np.array(A + list(rng.normal(size=(20000, 3)))); b = np.array(B + list(rng.normal(size=(20000, 3))))
+    n = np.array(N + list(rng.normal(size=(20000, 3))))
+    # nearly parallel / antiparallel pairs: the product y is a rounding residue of either sign or a signed zero
+    t = rng.normal(size=(20000, 3)); s = rng.choice([-1.0, 1.0, 2.0, -0.5], size=(20000, 1))
+    a = np.concatenate([a, t]); b = np.concatenate([b, t * s]); n = np.concatenate([n, rng.normal(size=(20000, 3))])
+    a, b, n = (np.ascontiguousarray(v, dtype=np.float64) for v in (a, b, n))
+    out = np.zeros(len(a), dtype=np.uint8)
+    p = lambda v: v.ctypes.data_as(C.c_void_p)
+    lib.hc_signed_angle_nonneg(C.c_int64(len(a)), p(a), p(b), p(n), p(out))
+    with np.errstate(all="ignore"):
+        cx = a[:, 1] * b[:, 2] - a[:, 2] * b[:, 1]
+        cy = a[:, 2] * b[:, 0] - a[:, 0] * b[:, 2]
+        cz = a[:, 0] * b[:, 1] - a[:, 1] * b[:, 0]
+        y = cx * n[:, 0] + cy * n[:, 1] + cz * n[:, 2]
+        x = a[:, 0] * b[:, 0] + a[:, 1] * b[:, 1] + a[:, 2] * b[:, 2]
+        want = (np.arctan2(y, x) >= 0).astype(np.uint8)
+    assert np.array_equal(out, want), np.flatnonzero(out != want)[:10]
+    assert 0 < want.sum() < len(want)
